@@ -1,0 +1,107 @@
+"""CPU oracle for the TW clustering hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / `--impl reference` legs may
+import this package.  The product path (paper_2412_12382_b200/) never imports it.
+
+The arithmetic lives in twc_oracle.c (plain C, see its header for the PAPER.md citations);
+this file only builds/loads it with ctypes and marshals numpy arrays.
+
+    score(g, rows=None)          -> (t, wedge, tw)   int32[m] each, canonical (u<v lex) order
+    cluster(g, tw, delta)        -> (labels int32[n], kept_edges, n_components)
+    sweep(g, tw, deltas)         -> list of cluster() results
+
+Every function is pinned in tests/test_oracle_pins.py against brute force, closed forms,
+invariants and library routines (scipy / networkx); see DESIGN.md "Oracle pins".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "twc_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile twc_oracle.c with gcc (-O2 -fopenmp).  Building the checker is not using it."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fopenmp", "-shared", "-fPIC",
+                               "-Wall", "-Wextra", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        I64 = ctypes.c_int64
+        lib.oracle_score.argtypes = [I64, P, P, I64, I64, P, P, P]
+        lib.oracle_score.restype = ctypes.c_int
+        lib.oracle_cluster.argtypes = [I64, P, P, P, ctypes.c_double, P, P]
+        lib.oracle_cluster.restype = ctypes.c_int
+        lib.oracle_max_threads.restype = ctypes.c_int
+        lib.oracle_set_threads.argtypes = [ctypes.c_int]
+        _lib = lib
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a.size else None
+
+
+def _csr(g):
+    rowptr = np.ascontiguousarray(g.rowptr, dtype=np.int64)
+    colidx = np.ascontiguousarray(g.colidx, dtype=np.int32)
+    return rowptr, colidx
+
+
+def set_threads(k: int) -> None:
+    _load().oracle_set_threads(int(k))
+
+
+def max_threads() -> int:
+    return int(_load().oracle_max_threads())
+
+
+def score(g, rows=None):
+    """Per-edge (t, wedge, TW) for every canonical edge, or only for the edges whose smaller
+    endpoint lies in rows=(u_begin, u_end) (other entries stay 0)."""
+    lib = _load()
+    rowptr, colidx = _csr(g)
+    m = int(rowptr[-1]) // 2 if g.n > 0 else 0
+    t = np.zeros(m, dtype=np.int32)
+    wedge = np.zeros(m, dtype=np.int32)
+    tw = np.zeros(m, dtype=np.int32)
+    u0, u1 = (0, g.n) if rows is None else rows
+    if m:
+        rc = lib.oracle_score(g.n, _ptr(rowptr), _ptr(colidx), int(u0), int(u1),
+                              _ptr(t), _ptr(wedge), _ptr(tw))
+        if rc:
+            raise MemoryError("oracle_score allocation failed")
+    return t, wedge, tw
+
+
+def cluster(g, tw, delta: float):
+    lib = _load()
+    rowptr, colidx = _csr(g)
+    tw = np.ascontiguousarray(tw, dtype=np.int32)
+    labels = np.empty(g.n, dtype=np.int32)
+    stats = np.zeros(2, dtype=np.int64)
+    rc = lib.oracle_cluster(g.n, _ptr(rowptr), _ptr(colidx), _ptr(tw), float(delta),
+                            _ptr(labels), _ptr(stats))
+    if rc:
+        raise MemoryError("oracle_cluster allocation failed")
+    return labels, int(stats[0]), int(stats[1])
+
+
+def sweep(g, tw, deltas):
+    return [cluster(g, tw, d) for d in deltas]

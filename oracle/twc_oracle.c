@@ -1,0 +1,162 @@
+/*
+ * twc_oracle.c -- plain, slow, obviously-correct CPU oracle for the TW clustering hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load, call or execute anything under oracle/.
+ * The product path (paper_2412_12382_b200/) never links, imports or calls this file and
+ * shares no code, header, table or helper with it.
+ *
+ * What it computes (citations are PAPER.md line numbers "P:n", SPEC.md "S:n"):
+ *   oracle_score   -- for every canonical edge (u,v), u<v, in lexicographic order (reading C5,
+ *                     S:66-69): one two-pointer merge over the FULL sorted lists N(u), N(v)
+ *                     (the paper's own per-edge method) that counts
+ *                       t     = |N(u) & N(v)|
+ *                       uni   = |N(u) | N(v)|  (counted directly, not via degrees)
+ *                       wedge = uni - t - 2
+ *                       TW    = t - wedge                          (Eq. 2)
+ *   oracle_cluster -- Alg. 1: keep edge e iff NOT (TW(e) < delta) (reading
+ *                     C4), then connected components by breadth-first search from every
+ *                     unlabelled vertex in ascending id order, so every vertex is labelled
+ *                     with the minimum id of its component (reading C6).
+ *
+ * Parallelism: the only parallelism is an OpenMP loop over rows in oracle_score (disjoint
+ * writes, deterministic).  Everything is int32/int64 integer arithmetic, so there is no
+ * rounding anywhere (reading C18).  The comparison (double)TW < delta is exact (|TW| < 2^53).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+void oracle_set_threads(int k) {
+#ifdef _OPENMP
+    if (k > 0) omp_set_num_threads(k);
+#else
+    (void)k;
+#endif
+}
+
+/* Canonical edge offsets: eoff[u] = number of edges (a,b), a<b, with a < u.  S:66-69. */
+static void canonical_offsets(int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                              int64_t *eoff) {
+    eoff[0] = 0;
+    for (int64_t u = 0; u < n; ++u) {
+        int64_t up = 0;
+        for (int64_t p = rowptr[u]; p < rowptr[u + 1]; ++p)
+            if (colidx[p] > u) ++up;
+        eoff[u + 1] = eoff[u] + up;
+    }
+}
+
+/*
+ * Score the canonical edges whose smaller endpoint u lies in [u_begin, u_end).
+ * t/wedge/tw are full-length (m) arrays indexed by canonical edge id; entries of other rows are
+ * left untouched.  Returns 0, or 1 when an allocation fails.
+ */
+int oracle_score(int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                 int64_t u_begin, int64_t u_end,
+                 int32_t *t, int32_t *wedge, int32_t *tw) {
+    if (n <= 0) return 0;
+    int64_t *eoff = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    if (!eoff) return 1;
+    canonical_offsets(n, rowptr, colidx, eoff);
+    if (u_begin < 0) u_begin = 0;
+    if (u_end > n) u_end = n;
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t u = u_begin; u < u_end; ++u) {
+        int64_t c = eoff[u];
+        for (int64_t p = rowptr[u]; p < rowptr[u + 1]; ++p) {
+            int64_t v = colidx[p];
+            if (v <= u) continue;                      /* canonical: u < v only */
+            /* one merge over N(u) and N(v): intersection and union sizes */
+            int64_t i = rowptr[u], ie = rowptr[u + 1];
+            int64_t j = rowptr[v], je = rowptr[v + 1];
+            int64_t inter = 0, uni = 0;
+            while (i < ie && j < je) {
+                int32_t a = colidx[i], b = colidx[j];
+                if (a == b) { ++inter; ++uni; ++i; ++j; }
+                else if (a < b) { ++uni; ++i; }
+                else { ++uni; ++j; }
+            }
+            uni += (ie - i) + (je - j);
+            int64_t wdg = uni - inter - 2;
+            t[c] = (int32_t)inter;
+            wedge[c] = (int32_t)wdg;
+            tw[c] = (int32_t)(inter - wdg);           /* Eq. 2 */
+            ++c;
+        }
+    }
+    free(eoff);
+    return 0;
+}
+
+/*
+ * Alg. 1 for one threshold.  labels[n] receives the minimum vertex id of each vertex's
+ * component in the kept subgraph; stats (may be NULL) receives {kept_edges, n_components}.
+ * Returns 0, or 1 when an allocation fails.
+ */
+int oracle_cluster(int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                   const int32_t *tw, double delta, int32_t *labels, int64_t *stats) {
+    if (n <= 0) {
+        if (stats) { stats[0] = 0; stats[1] = 0; }
+        return 0;
+    }
+    /* line 1 of Alg. 1: remove e iff sim(e) < delta -- materialise the kept graph */
+    int64_t *kdeg = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    if (!kdeg) return 1;
+    int64_t c = 0, kept = 0;
+    for (int64_t u = 0; u < n; ++u)
+        for (int64_t p = rowptr[u]; p < rowptr[u + 1]; ++p) {
+            int64_t v = colidx[p];
+            if (v <= u) continue;
+            if (!((double)tw[c] < delta)) { kdeg[u + 1]++; kdeg[v + 1]++; ++kept; }
+            ++c;
+        }
+    for (int64_t u = 0; u < n; ++u) kdeg[u + 1] += kdeg[u];
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    int32_t *kadj = (int32_t *)malloc(sizeof(int32_t) * (size_t)(2 * kept + 1));
+    int32_t *queue = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    if (!fill || !kadj || !queue) { free(kdeg); free(fill); free(kadj); free(queue); return 1; }
+    memcpy(fill, kdeg, sizeof(int64_t) * (size_t)n);
+    c = 0;
+    for (int64_t u = 0; u < n; ++u)
+        for (int64_t p = rowptr[u]; p < rowptr[u + 1]; ++p) {
+            int64_t v = colidx[p];
+            if (v <= u) continue;
+            if (!((double)tw[c] < delta)) {
+                kadj[fill[u]++] = (int32_t)v;
+                kadj[fill[v]++] = (int32_t)u;
+            }
+            ++c;
+        }
+    /* line 2 of Alg. 1: connected components, by BFS in ascending start id */
+    for (int64_t u = 0; u < n; ++u) labels[u] = -1;
+    int64_t ncomp = 0;
+    for (int64_t s = 0; s < n; ++s) {
+        if (labels[s] >= 0) continue;
+        ++ncomp;
+        int64_t head = 0, tail = 0;
+        labels[s] = (int32_t)s;
+        queue[tail++] = (int32_t)s;
+        while (head < tail) {
+            int32_t x = queue[head++];
+            for (int64_t p = kdeg[x]; p < kdeg[x + 1]; ++p) {
+                int32_t y = kadj[p];
+                if (labels[y] < 0) { labels[y] = (int32_t)s; queue[tail++] = y; }
+            }
+        }
+    }
+    if (stats) { stats[0] = kept; stats[1] = ncomp; }
+    free(kdeg); free(fill); free(kadj); free(queue);
+    return 0;
+}
