@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""bench.py -- TW scoring + threshold sweep (arXiv 2412.12382, Alg. 1 with Eq. 2) on B200.
+
+One step = the whole hot path on BASELINE config 5 (DC-SBM,
+n = 4,000,000, m ~ 35M, int64 rowptr): twc_score (orientation, intersection, fused score
+epilogue) followed by twc_sweep over the 16 thresholds -30, -28, ..., 0 reusing the
+scores (filter + connected components per threshold).  Inputs are resident in HBM when the
+timed region starts; `e2e` times the same step through twc_pipeline_host from pinned host
+buffers (H2D of the CSR, D2H of TW + labels + stats inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
+
+N > 1 runs under torchrun: every rank scores its own replica of the workload (independent
+problems, no data-path collective, "scaling": "weak").  --impl reference
+times the CPU oracle (oracle/, test infrastructure) on bounded samples of the same workload.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import graphgen as gg  # noqa: E402
+import harness  # noqa: E402
+
+METRIC = "edges scored/sec (TW) and end-to-end cluster time; achieved HBM GB/s vs peak"
+UNIT = "edges/s"
+L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def workload_desc(cfg, g, k):
+    c = gg.CONFIGS[cfg]
+    kind = "planted-partition SBM" if c["kind"] == "pp" else "degree-corrected SBM"
+    return (f"config{cfg}: {kind} n={g.n} m={g.m} (BASELINE.json configs[{cfg - 1}], seed "
+            f"{c['seed']}); step = twc_score + {k}-threshold twc_sweep (filter + CC)")
+
+
+# ----------------------------------------------------------------------------- host stats
+def orientation_stats(g):
+    """Sum_v d-(v) d+(v) for the degree orientation (the pivot-staged intersection volume)."""
+    rp = g.rowptr.astype(np.int64)
+    deg = np.diff(rp)
+    src = np.repeat(np.arange(g.n, dtype=np.int64), deg)
+    dst = g.colidx.astype(np.int64)
+    out = (deg[src] < deg[dst]) | ((deg[src] == deg[dst]) & (src < dst))
+    dplus = np.bincount(src[out], minlength=g.n).astype(np.int64)
+    dminus = deg - dplus
+    return int((dminus * dplus).sum()), int(dplus.max()) if g.n else 0
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "k2_ncu_summary.json")
+    try:
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_launch"), d
+    except Exception:
+        return None, None
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            time.sleep(0.1)
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+
+
+# ----------------------------------------------------------------------------- CPU oracle arm
+def oracle_samples(g, cfg, n_windows=64):
+    """Bounded samples of the workload for the oracle: the canonical edges of a window of rows,
+    plus the subgraph those edges form (compactly relabelled, order-preserving) for the
+    filter + connected-components part.  Harness bookkeeping only, untimed."""
+    s, d = g.canonical_pairs()
+    bounds = np.linspace(0, g.n, n_windows + 1).astype(np.int64)
+    edge_lo = np.searchsorted(s, bounds[:-1], side="left")
+    edge_hi = np.searchsorted(s, bounds[1:], side="left")
+    out = []
+    for w in range(n_windows):
+        a, b = int(edge_lo[w]), int(edge_hi[w])
+        ss, dd = s[a:b], d[a:b]
+        verts = np.unique(np.concatenate([ss, dd]))
+        sub = gg.csr_from_pairs(int(verts.size), np.searchsorted(verts, ss),
+                                np.searchsorted(verts, dd))
+        out.append((int(bounds[w]), int(bounds[w + 1]), a, b, sub))
+    return out
+
+
+def oracle_step(oracle, g, sample, deltas):
+    r0, r1, a, b, sub = sample
+    t0 = time.perf_counter()
+    _, _, tw = oracle.score(g, rows=(r0, r1))
+    tws = tw[a:b]
+    for dlt in deltas:
+        oracle.cluster(sub, tws, dlt)
+    return b - a, time.perf_counter() - t0
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_cpu_baseline(g, cfg, deltas, seconds):
+    import oracle
+    oracle.build()
+    cores = cpu_cores()
+    oracle.set_threads(cores)
+    samples = oracle_samples(g, cfg)
+    edges = 0
+    secs = 0.0
+    used = 0
+    for smp in samples:
+        e, dt = oracle_step(oracle, g, smp, deltas)
+        edges += e
+        secs += dt
+        used += 1
+        if secs >= seconds:
+            break
+    return {"value": edges / secs if secs > 0 else None, "unit": UNIT, "cores": cores,
+            "kind": "oracle",
+            "sample": (f"{used} of 64 row windows of config {cfg} ({edges} canonical edges, "
+                       f"{secs:.1f} s): oracle per-edge full-list merge scoring (OpenMP, "
+                       f"{cores} threads) + {len(deltas)}-threshold filter + BFS labelling of "
+                       f"the windows' edges (single thread)")}
+
+
+def main_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = args.config
+    g = gg.config_graph(cfg)
+    import oracle
+    oracle.build()
+    cores = cpu_cores()
+    oracle.set_threads(cores)
+    _, _, tw_full = (None, None, None)
+    deltas = harness.SWEEP_GRID if cfg == 5 else None
+    if deltas is None:
+        _, _, tw_full = oracle.score(g)
+        deltas = harness.thresholds(cfg, tw_full)
+    samples = oracle_samples(g, cfg)
+    for i in range(args.warmup):
+        oracle_step(oracle, g, samples[i % len(samples)], deltas)
+    edges = 0
+    secs = 0.0
+    for i in range(args.steps):
+        e, dt = oracle_step(oracle, g, samples[(args.warmup + i) % len(samples)], deltas)
+        edges += e
+        secs += dt
+    value = edges / secs
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * secs / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg, g, len(deltas)), "n": g.n, "m": g.m,
+                       "graph_sha256": g.sha256(), "parallelism": "cpu oracle"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": (f"each step = one of 64 row windows of config {cfg}: "
+                                        "oracle scoring of the window's canonical edges + "
+                                        f"{len(deltas)}-threshold filter + BFS on those edges")},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- B200 arm
+def main_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_12382_b200 as twc
+    from paper_2412_12382_b200 import build as twc_build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        twc_build.build()
+    if world > 1:
+        dist.barrier()
+    twc.load_library()
+
+    cfg = args.config
+    g = gg.config_graph(cfg)
+    n, m = g.n, g.m
+    rp, ci = harness.to_device(g, dev)
+    rb = rp.element_size()
+    stream = torch.cuda.current_stream()
+    ws_s = torch.empty(twc.twc_score_workspace_bytes(n, m, rb), dtype=torch.uint8, device=dev)
+    ws_c = torch.empty(twc.twc_cluster_workspace_bytes(n, m, rb), dtype=torch.uint8, device=dev)
+    t, w, tw = (torch.empty(m, dtype=torch.int32, device=dev) for _ in range(3))
+    twc.twc_score(rp, ci, out=(t, w, tw), workspace=ws_s)
+    torch.cuda.synchronize()
+    deltas = harness.thresholds(cfg, tw.cpu().numpy())
+    k = len(deltas)
+    labels = torch.empty((k, n), dtype=torch.int32, device=dev)
+    stats = torch.empty((k, 2), dtype=torch.int64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def mk(nev):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+        for e in evs:
+            e.record(stream)
+        return evs
+
+    def step(se=None, we=None):
+        twc.twc_score(rp, ci, out=(t, w, tw), workspace=ws_s, events=se)
+        twc.twc_sweep(rp, ci, tw, deltas, labels=labels, stats=stats, workspace=ws_c, events=we)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    sev = [mk(4) for _ in range(K)]
+    wev = [mk(3) for _ in range(K)]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    torch.cuda.synchronize()
+    l0 = twc.twc_kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        wall0 = time.perf_counter()
+        for i in range(K):
+            flush.zero_()                      # L2 flush between timed steps (not timed)
+            starts[i].record(stream)
+            step(sev[i], wev[i])
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    launches = (twc.twc_kernel_launches() - l0) / K
+    step_ms = [starts[i].elapsed_time(ends[i]) for i in range(K)]
+    prep_ms = [sev[i][0].elapsed_time(sev[i][1]) for i in range(K)]
+    k2_ms = [sev[i][1].elapsed_time(sev[i][2]) for i in range(K)]
+    k3_ms = [sev[i][2].elapsed_time(sev[i][3]) for i in range(K)]
+    score_ms = [sev[i][0].elapsed_time(sev[i][3]) for i in range(K)]
+    sweep_ms = [wev[i][0].elapsed_time(wev[i][2]) for i in range(K)]
+    total_s = sum(step_ms) / 1000.0
+    if world > 1:
+        tt = torch.tensor([total_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_s = float(tt.item())
+    value = world * m * K / total_s
+    ms_per_step = 1000.0 * total_s / K
+
+    # ---- roofline of the dominant kernel (K2, oriented intersection), DESIGN.md Sec. 5
+    S, dplus_max = orientation_stats(g)
+    T = int(t.sum(dtype=torch.int64).item()) // 3
+    k2_bytes = 4 * (n + 1 + 4 * m + S + T)
+    k2_avg_s = statistics.mean(k2_ms) / 1000.0
+    peak, peak_src = measured_peak()
+    achieved = k2_bytes / k2_avg_s / 1e9
+    traffic, _ = ncu_traffic()
+    roofline = {"bound": "hbm", "kernel": "k2_intersect", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "algorithmic_bytes_per_launch": k2_bytes, "peak_source": peak_src,
+                "k2_ms_avg": 1000 * k2_avg_s}
+
+    # ---- end to end through the public host API
+    e2e = None
+    if not args.no_e2e:
+        rp_h = torch.from_numpy(np.ascontiguousarray(g.rowptr)).pin_memory()
+        ci_h = torch.from_numpy(np.ascontiguousarray(g.colidx)).pin_memory()
+        out_h = {"tw": torch.empty(m, dtype=torch.int32, pin_memory=True),
+                 "labels": torch.empty((k, n), dtype=torch.int32, pin_memory=True),
+                 "stats": torch.empty((k, 2), dtype=torch.int64, pin_memory=True)}
+        ws_p = torch.empty(twc.twc_pipeline_workspace_bytes(n, m, rb, k), dtype=torch.uint8,
+                           device=dev)
+        for _ in range(2):
+            twc.twc_pipeline_host(rp_h, ci_h, deltas, out=out_h, workspace=ws_p, device=dev)
+        if world > 1:
+            dist.barrier()
+        e_times = []
+        for _ in range(max(3, min(K, 10))):
+            t0 = time.perf_counter()
+            twc.twc_pipeline_host(rp_h, ci_h, deltas, out=out_h, workspace=ws_p, device=dev)
+            e_times.append(time.perf_counter() - t0)
+        e_s = sum(e_times) / len(e_times)
+        if world > 1:
+            tt = torch.tensor([e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_s = float(tt.item())
+        assert torch.equal(out_h["tw"], tw.cpu()) and torch.equal(out_h["labels"], labels.cpu())
+        e2e = {"value": world * m / e_s, "unit": UNIT,
+               "h2d_bytes_per_step": rp_h.numel() * rp_h.element_size() + ci_h.numel() * 4,
+               "d2h_bytes_per_step": 4 * m + 4 * k * n + 16 * k, "ms_per_step": 1000 * e_s}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = run_cpu_baseline(g, cfg, deltas, args.cpu_seconds)
+
+    csum = clk.summary()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg, g, k), "n": n, "m": m, "thresholds": deltas,
+                       "rowptr": str(g.rowptr.dtype), "graph_sha256": g.sha256(),
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "explicit 512 MiB L2 flush between timed steps; inputs (CSR 312 MB) "
+                             "and outputs exceed the 126 MB L2"},
+            "phases_ms": {"score": statistics.mean(score_ms), "orient": statistics.mean(prep_ms),
+                          "intersect_k2": statistics.mean(k2_ms), "epilogue_k3": statistics.mean(k3_ms),
+                          "sweep16": statistics.mean(sweep_ms)},
+            "score_edges_per_s": world * m / (statistics.mean(score_ms) / 1000.0),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": csum, "wall_s_timed": wall,
+            "graph": {"triangles": T, "sum_dminus_dplus": S, "max_dplus": dplus_max,
+                      "max_degree": int(np.diff(g.rowptr.astype(np.int64)).max())}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return main_reference(args)
+    return main_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

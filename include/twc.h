@@ -1,0 +1,156 @@
+/*
+ * twc.h -- C ABI of the B200 triangle/wedge (TW) edge-scoring and motif-based clustering path
+ * (arXiv 2412.12382, Chen & Tsourakakis).  Citations: "P:n" = PAPER.md line n, "S:n" = SPEC.md
+ * line n, "SURVEY x" = SURVEY.md section.  Implemented by libtwc.so
+ * (paper_2412_12382_b200/csrc/); sm_100a only.
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  Graph.   twc_csr describes an undirected simple graph in CSR form with DEVICE pointers
+ *           (for the *_host calls, HOST pointers): rowptr has n+1 entries of rowptr_bytes
+ *           (4 = int32, 8 = int64) bytes with rowptr[0] = 0 and rowptr[n] = 2m; colidx has 2m
+ *           int32 entries; every row is strictly increasing, the graph is symmetric and has
+ *           no self-loops (the paper's pre-processing "sort the adjacency list by node id",
+ *           P:618).  Limits: 0 <= n < 2^31, 0 <= m < 2^31.  The precondition is NOT
+ *           checked by the scoring calls (the wedge closed form assumes it); twc_validate_csr
+ *           checks it.
+ *  Edges.   Per-edge outputs are indexed by the canonical edge id: the edges (u,v), u<v, in
+ *           lexicographic order (reading C5), i.e. the upper
+ *           triangle of the CSR in row order.
+ *  Memory.  Every array is caller-owned.  The library never allocates device memory: all
+ *           scratch comes from a caller-provided device workspace whose size is given by the
+ *           matching *_workspace_bytes query (cuBLAS style).  Workspaces must be 256-byte
+ *           aligned.  Nothing is retained after a call returns; outputs must not alias inputs.
+ *  Streams. `stream` is a cudaStream_t (NULL = legacy default stream).  Device calls only
+ *           enqueue work on it and return without synchronising (outputs are valid once the
+ *           stream reaches them), except twc_validate_csr and the *_host calls, which
+ *           synchronise the stream before returning.
+ *  Errors.  Calls return a twc_status.  TWC_EINVAL: a null pointer where data is required
+ *           (n > 0 or m > 0), n or m out of range, rowptr_bytes not in {4, 8}, NaN delta,
+ *           k < 1.  TWC_EWORKSPACE: workspace too small or misaligned.  TWC_ECUDA: a CUDA launch
+ *           or runtime error (detail in twc_last_error()).  TWC_EGRAPH: only from
+ *           twc_validate_csr.  Outputs are undefined on error; nothing aborts or throws.
+ *           n = 0 or m = 0 is not an error: empty score arrays; labels[u] = u.
+ *  Threads. Calls are re-entrant; there is no global state except the thread-local error
+ *           string returned by twc_last_error().
+ */
+#ifndef TWC_H_
+#define TWC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TWC_OK = 0,
+    TWC_EINVAL = 1,
+    TWC_EWORKSPACE = 2,
+    TWC_ECUDA = 3,
+    TWC_EGRAPH = 4
+} twc_status;
+
+typedef struct {
+    int64_t n;             /* vertices, 0 <= n < 2^31                                        */
+    int64_t m;             /* undirected edges; rowptr[n] == 2m, 0 <= m < 2^31              */
+    const void *rowptr;    /* n+1 entries of rowptr_bytes each                               */
+    int32_t rowptr_bytes;  /* 4 (int32) or 8 (int64)                                          */
+    const int32_t *colidx; /* 2m entries                                                      */
+} twc_csr;
+
+/* ---------------------------------------------------------------------------------------
+ * twc_score -- per-edge triangle count, wedge count and TW score.
+ *
+ *   t[e]     = |N(u) & N(v)|                                  ("Notations")
+ *   wedge[e] = |N(u) | N(v)| - |N(u) & N(v)| - 2
+ *   tw[e]    = t[e] - wedge[e]                                (Eq. 2)
+ * for every canonical edge e = (u,v).  t, wedge, tw: device int32[m] each, written in full.
+ * Exact integers (no rounding).  Needs a workspace of twc_score_workspace_bytes(n, m, rb).
+ * ------------------------------------------------------------------------------------- */
+size_t twc_score_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes);
+twc_status twc_score(const twc_csr *g, void *workspace, size_t workspace_bytes,
+                     int32_t *t, int32_t *wedge, int32_t *tw, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * twc_cluster -- Alg. 1 for one threshold on precomputed scores.
+ *
+ * Removes every edge e with tw[e] < delta (equality is kept, reading C4;
+ * the comparison (double)tw[e] < delta is exact) and labels the connected components of the
+ * remaining graph: labels[u] = the minimum vertex id of u's component (S:208-210,
+ * S:228; isolated vertices are singletons).  delta may be +-infinity, not NaN.
+ *   tw:     device int32[m], canonical order (e.g. from twc_score).
+ *   labels: device int32[n], written in full.
+ *   stats:  device int64[2] = {kept_edges, n_components}, or NULL.
+ * Needs a workspace of twc_cluster_workspace_bytes(n, m, rb).
+ * ------------------------------------------------------------------------------------- */
+size_t twc_cluster_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes);
+twc_status twc_cluster(const twc_csr *g, const int32_t *tw, double delta, void *workspace,
+                       size_t workspace_bytes, int32_t *labels, int64_t *stats, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * twc_sweep -- twc_cluster for k thresholds reusing one score array (
+ * S:384 "computed once per sweep ... T cheap CC passes").  Results equal k independent
+ * twc_cluster calls.  deltas_host: HOST double[k] (any order, no NaN).  labels: device
+ * int32[k*n], labels[i*n + u] for deltas_host[i].  stats: device int64[2k] or NULL.
+ * Same workspace size as twc_cluster.
+ * ------------------------------------------------------------------------------------- */
+twc_status twc_sweep(const twc_csr *g, const int32_t *tw, const double *deltas_host, int32_t k,
+                     void *workspace, size_t workspace_bytes, int32_t *labels, int64_t *stats,
+                     void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * twc_pipeline_host -- the whole path end to end from HOST buffers: copies the CSR to the
+ * device, runs twc_score then twc_sweep over deltas_host[k], copies the results back and
+ * synchronises the stream.  g points at HOST rowptr/colidx (pinned memory gives full PCIe
+ * speed; pageable works).  t, wedge, tw: HOST int32[m] each, or NULL to skip that copy-back.
+ * labels: HOST int32[k*n] or NULL.  stats: HOST int64[2k] or NULL.  Needs a DEVICE workspace
+ * of twc_pipeline_workspace_bytes(n, m, rb, k) (holds the device copies too).
+ * ------------------------------------------------------------------------------------- */
+size_t twc_pipeline_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes, int32_t k);
+twc_status twc_pipeline_host(const twc_csr *g_host, const double *deltas_host, int32_t k,
+                             void *workspace, size_t workspace_bytes, int32_t *t, int32_t *wedge,
+                             int32_t *tw, int32_t *labels, int64_t *stats, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * twc_validate_csr -- checks the a0 precondition: rowptr[0] = 0, rowptr
+ * non-decreasing, rowptr[n] = 2m, 0 <= colidx < n, rows strictly increasing, no self-loops,
+ * symmetry.  Writes a bit mask to *verdict (device int32; 0 = valid; bit 0 rowptr, bit 1 id
+ * range, bit 2 order/duplicates, bit 3 self-loop, bit 4 asymmetry), synchronises the stream
+ * and returns TWC_OK when valid, TWC_EGRAPH otherwise.  Workspace: none needed (may be NULL).
+ * ------------------------------------------------------------------------------------- */
+twc_status twc_validate_csr(const twc_csr *g, int32_t *verdict, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Instrumented variants (bench.py): identical results to twc_score / twc_sweep.  `events` is
+ * NULL or an array of caller-created cudaEvent_t handles that the call records on `stream` at
+ * its phase boundaries, so the caller can time each phase with cudaEventElapsedTime:
+ *   twc_score_ex: TWC_SCORE_NEVENTS = 4 events -- [0] start, [1] orientation done (K0, K1,
+ *                 scans), [2] intersection done (K2), [3] epilogue done (K3).
+ *   twc_sweep_ex: TWC_SWEEP_NEVENTS = 3 events -- [0] start, [1] setup done, [2] all k
+ *                 thresholds filtered + labelled.
+ * ------------------------------------------------------------------------------------- */
+#define TWC_SCORE_NEVENTS 4
+#define TWC_SWEEP_NEVENTS 3
+twc_status twc_score_ex(const twc_csr *g, void *workspace, size_t workspace_bytes, int32_t *t,
+                        int32_t *wedge, int32_t *tw, void *stream, void *const *events);
+twc_status twc_sweep_ex(const twc_csr *g, const int32_t *tw, const double *deltas_host,
+                        int32_t k, void *workspace, size_t workspace_bytes, int32_t *labels,
+                        int64_t *stats, void *stream, void *const *events);
+
+/* Number of kernels this process has launched through the library so far (monotone counter;
+ * bench.py reports the per-step difference as gpu_launches). */
+int64_t twc_kernel_launches(void);
+
+/* Static description of a status code; never NULL. */
+const char *twc_status_string(twc_status s);
+/* Detail of this thread's last non-OK status ("" if none); valid until the next call. */
+const char *twc_last_error(void);
+/* ABI version: 100 * major + minor. */
+int32_t twc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TWC_H_ */

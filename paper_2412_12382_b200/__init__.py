@@ -1,0 +1,239 @@
+"""paper_2412_12382_b200 -- B200 (sm_100a) triangle/wedge (TW) edge scoring and motif-based
+clustering (arXiv 2412.12382, Alg. 1 with the TW score of Eq. 2).
+
+Thin ctypes binding over libtwc.so (include/twc.h): argument marshalling only; every step of
+the path runs in the library's CUDA kernels.  PyTorch supplies device memory and streams.
+There is no CPU fallback: if libtwc.so is missing or no CUDA device is present, calls raise.
+
+    t, wedge, tw      = twc_score(rowptr, colidx)                  # device int32[m] each
+    labels, stats     = twc_cluster(rowptr, colidx, tw, delta)     # int32[n], int64[2]
+    labels, stats     = twc_sweep(rowptr, colidx, tw, deltas)      # int32[k, n], int64[k, 2]
+    out               = twc_pipeline_host(rowptr_h, colidx_h, deltas)   # host in, host out
+    twc_validate_csr(rowptr, colidx)                                # raises TwcError if invalid
+
+rowptr: int32 or int64 tensor [n+1]; colidx: int32 tensor [2m] (CUDA tensors, except for
+twc_pipeline_host which takes CPU tensors, ideally pinned).  Outputs are in canonical edge
+order: the edges (u, v), u < v, lexicographically.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtwc.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "twc.h")
+
+TWC_OK, TWC_EINVAL, TWC_EWORKSPACE, TWC_ECUDA, TWC_EGRAPH = range(5)
+
+
+class TwcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[{status}] {msg}")
+        self.status = status
+
+
+class _Csr(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("m", ctypes.c_int64), ("rowptr", ctypes.c_void_p),
+                ("rowptr_bytes", ctypes.c_int32), ("colidx", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libtwc.so (raises OSError loudly when it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise OSError(f"{path} not found: build it with `python -m paper_2412_12382_b200.build` "
+                      "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P, I64, I32, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+    CP = ctypes.POINTER(_Csr)
+    sig = {
+        "twc_score_workspace_bytes": (SZ, [I64, I64, I32]),
+        "twc_score": (ctypes.c_int, [CP, P, SZ, P, P, P, P]),
+        "twc_cluster_workspace_bytes": (SZ, [I64, I64, I32]),
+        "twc_cluster": (ctypes.c_int, [CP, P, ctypes.c_double, P, SZ, P, P, P]),
+        "twc_sweep": (ctypes.c_int, [CP, P, P, I32, P, SZ, P, P, P]),
+        "twc_pipeline_workspace_bytes": (SZ, [I64, I64, I32, I32]),
+        "twc_pipeline_host": (ctypes.c_int, [CP, P, I32, P, SZ, P, P, P, P, P, P]),
+        "twc_validate_csr": (ctypes.c_int, [CP, P, P]),
+        "twc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+        "twc_last_error": (ctypes.c_char_p, []),
+        "twc_version": (I32, []),
+        "twc_score_ex": (ctypes.c_int, [CP, P, SZ, P, P, P, P, P]),
+        "twc_sweep_ex": (ctypes.c_int, [CP, P, P, I32, P, SZ, P, P, P, P]),
+        "twc_kernel_launches": (I64, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def header_functions(path: str = HEADER_PATH):
+    """Names of every function include/twc.h declares (for the ABI export test)."""
+    txt = open(path).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(twc_[a-z_]+)\s*\(", txt)))
+
+
+def _check(status: int):
+    if status != TWC_OK:
+        lib = load_library()
+        raise TwcError(status, f"{lib.twc_status_string(status).decode()}: "
+                               f"{lib.twc_last_error().decode()}")
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() else None
+
+
+def _graph(rowptr, colidx, need_cuda=True):
+    if rowptr.dtype not in (torch.int32, torch.int64) or colidx.dtype != torch.int32:
+        raise TypeError("rowptr must be int32/int64 and colidx int32")
+    if need_cuda and (not rowptr.is_cuda or not colidx.is_cuda):
+        raise ValueError("rowptr/colidx must be CUDA tensors")
+    if not rowptr.is_contiguous() or not colidx.is_contiguous():
+        raise ValueError("rowptr/colidx must be contiguous")
+    n = rowptr.numel() - 1
+    m = colidx.numel() // 2
+    g = _Csr(n, m, _ptr(rowptr) if n >= 0 else None, rowptr.element_size(), _ptr(colidx))
+    return g, n, m
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _workspace(nbytes, device, workspace=None):
+    if workspace is not None and workspace.numel() >= nbytes:
+        return workspace
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def twc_score_workspace_bytes(n, m, rowptr_bytes=4):
+    return int(load_library().twc_score_workspace_bytes(n, m, rowptr_bytes))
+
+
+def twc_cluster_workspace_bytes(n, m, rowptr_bytes=4):
+    return int(load_library().twc_cluster_workspace_bytes(n, m, rowptr_bytes))
+
+
+def twc_pipeline_workspace_bytes(n, m, rowptr_bytes=4, k=1):
+    return int(load_library().twc_pipeline_workspace_bytes(n, m, rowptr_bytes, k))
+
+
+def _events(events):
+    """torch.cuda.Event list -> C array of cudaEvent_t (events must already exist: record once)."""
+    if events is None:
+        return None
+    arr = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
+    return ctypes.cast(arr, ctypes.c_void_p), arr
+
+
+def twc_kernel_launches():
+    return int(load_library().twc_kernel_launches())
+
+
+def twc_score(rowptr, colidx, out=None, workspace=None, stream=None, events=None):
+    """Per-edge (t, wedge, TW) -- P:337 and Eq. 2 -- for every canonical edge.
+
+    events: optional list of 4 torch.cuda.Event recorded at the phase boundaries
+    (TWC_SCORE_NEVENTS, include/twc.h)."""
+    lib = load_library()
+    g, n, m = _graph(rowptr, colidx)
+    dev = colidx.device
+    if out is None:
+        out = tuple(torch.empty(m, dtype=torch.int32, device=dev) for _ in range(3))
+    t, wedge, tw = out
+    ws = _workspace(lib.twc_score_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    ev = _events(events)
+    _check(lib.twc_score_ex(ctypes.byref(g), _ptr(ws), ws.numel(), _ptr(t), _ptr(wedge), _ptr(tw),
+                            _stream(stream), ev[0] if ev else None))
+    return t, wedge, tw
+
+
+def twc_cluster(rowptr, colidx, tw, delta, labels=None, stats=None, workspace=None, stream=None):
+    """Alg. 1 at one threshold: labels[u] = min vertex id of u's component."""
+    lib = load_library()
+    g, n, m = _graph(rowptr, colidx)
+    dev = colidx.device
+    if labels is None:
+        labels = torch.empty(n, dtype=torch.int32, device=dev)
+    if stats is None:
+        stats = torch.empty(2, dtype=torch.int64, device=dev)
+    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    _check(lib.twc_cluster(ctypes.byref(g), _ptr(tw), float(delta), _ptr(ws), ws.numel(),
+                           _ptr(labels), _ptr(stats), _stream(stream)))
+    return labels, stats
+
+
+def twc_sweep(rowptr, colidx, tw, deltas, labels=None, stats=None, workspace=None, stream=None,
+              events=None):
+    """Alg. 1 for k thresholds reusing the scores: labels[i] for deltas[i].
+
+    events: optional list of 3 torch.cuda.Event (TWC_SWEEP_NEVENTS, include/twc.h)."""
+    lib = load_library()
+    g, n, m = _graph(rowptr, colidx)
+    dev = colidx.device
+    deltas = [float(d) for d in deltas]
+    k = len(deltas)
+    if labels is None:
+        labels = torch.empty((k, n), dtype=torch.int32, device=dev)
+    if stats is None:
+        stats = torch.empty((k, 2), dtype=torch.int64, device=dev)
+    arr = (ctypes.c_double * k)(*deltas)
+    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    ev = _events(events)
+    _check(lib.twc_sweep_ex(ctypes.byref(g), _ptr(tw), ctypes.cast(arr, ctypes.c_void_p), k,
+                            _ptr(ws), ws.numel(), _ptr(labels), _ptr(stats), _stream(stream),
+                            ev[0] if ev else None))
+    return labels, stats
+
+
+def twc_pipeline_host(rowptr, colidx, deltas, want_scores=True, out=None, workspace=None,
+                      stream=None, device=None):
+    """Host CSR in, host results out: H2D copy, score, sweep, D2H copy, sync (one C call).
+
+    rowptr/colidx: CPU tensors (pinned for full PCIe speed).  Returns dict with host tensors
+    t, wedge, tw (if want_scores), labels [k, n] and stats [k, 2]."""
+    lib = load_library()
+    g, n, m = _graph(rowptr, colidx, need_cuda=False)
+    deltas = [float(d) for d in deltas]
+    k = len(deltas)
+    dev = torch.device("cuda") if device is None else torch.device(device)
+    if out is None:
+        pin = torch.cuda.is_available()
+        out = {"labels": torch.empty((k, n), dtype=torch.int32, pin_memory=pin),
+               "stats": torch.empty((k, 2), dtype=torch.int64, pin_memory=pin)}
+        if want_scores:
+            for key in ("t", "wedge", "tw"):
+                out[key] = torch.empty(m, dtype=torch.int32, pin_memory=pin)
+    arr = (ctypes.c_double * k)(*deltas)
+    ws = _workspace(lib.twc_pipeline_workspace_bytes(n, m, rowptr.element_size(), k), dev,
+                    workspace)
+    _check(lib.twc_pipeline_host(ctypes.byref(g), ctypes.cast(arr, ctypes.c_void_p), k,
+                                 _ptr(ws), ws.numel(), _ptr(out.get("t")), _ptr(out.get("wedge")),
+                                 _ptr(out.get("tw")), _ptr(out["labels"]), _ptr(out["stats"]),
+                                 _stream(stream)))
+    return out
+
+
+def twc_validate_csr(rowptr, colidx, stream=None):
+    """Raise TwcError(TWC_EGRAPH) unless the CSR is symmetric, sorted, loop-free (row a0)."""
+    lib = load_library()
+    g, n, m = _graph(rowptr, colidx)
+    verdict = torch.zeros(1, dtype=torch.int32, device=colidx.device)
+    _check(lib.twc_validate_csr(ctypes.byref(g), _ptr(verdict), _stream(stream)))
+    return 0

@@ -1,0 +1,312 @@
+// twc_api.cu -- the extern "C" boundary declared in include/twc.h: argument checks, workspace
+// carving, dtype dispatch (int32 / int64 rowptr) and error reporting.  No compute here.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+
+#include "twc.h"
+#include "twc_internal.h"
+
+namespace twc {
+
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+void count_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+static twc_status fail(twc_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+static twc_status cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return TWC_OK;
+    return fail(TWC_ECUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+int num_sms() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v <= 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            v = 148;
+        cache[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
+static twc_status check_csr(const twc_csr* g, bool need_ptrs = true) {
+    if (!g) return fail(TWC_EINVAL, "graph descriptor is NULL");
+    if (g->n < 0 || g->n >= ((int64_t)1 << 31)) return fail(TWC_EINVAL, "n=%lld out of range", (long long)g->n);
+    if (g->m < 0 || g->m >= ((int64_t)1 << 31)) return fail(TWC_EINVAL, "m=%lld out of range", (long long)g->m);
+    if (g->rowptr_bytes != 4 && g->rowptr_bytes != 8)
+        return fail(TWC_EINVAL, "rowptr_bytes=%d must be 4 or 8", g->rowptr_bytes);
+    if (g->rowptr_bytes == 4 && 2 * g->m >= ((int64_t)1 << 31))
+        return fail(TWC_EINVAL, "2m=%lld does not fit an int32 rowptr", (long long)(2 * g->m));
+    if (g->m > 0 && g->n == 0) return fail(TWC_EINVAL, "m > 0 with n == 0");
+    if (need_ptrs && g->n > 0 && !g->rowptr) return fail(TWC_EINVAL, "rowptr is NULL");
+    if (need_ptrs && g->m > 0 && !g->colidx) return fail(TWC_EINVAL, "colidx is NULL");
+    return TWC_OK;
+}
+
+static twc_status check_ws(void* ws, size_t have, size_t need) {
+    if (need == 0) return TWC_OK;
+    if (!ws) return fail(TWC_EWORKSPACE, "workspace is NULL (need %zu bytes)", need);
+    if (reinterpret_cast<uintptr_t>(ws) % kAlign)
+        return fail(TWC_EWORKSPACE, "workspace not %zu-byte aligned", kAlign);
+    if (have < need) return fail(TWC_EWORKSPACE, "workspace %zu bytes < required %zu", have, need);
+    return TWC_OK;
+}
+
+// keep iff NOT(tw < delta)  <=>  tw >= ceil(delta) for integer tw (reading C4 / C18)
+static twc_status delta_to_thr(double delta, long long* thr) {
+    const long long kBig = (long long)1 << 62;
+    if (isnan(delta)) return fail(TWC_EINVAL, "delta is NaN");
+    if (delta == -INFINITY) { *thr = -kBig; return TWC_OK; }
+    if (delta == INFINITY) { *thr = kBig; return TWC_OK; }
+    double c = ceil(delta);
+    if (c < -4.0e18) *thr = -kBig;
+    else if (c > 4.0e18) *thr = kBig;
+    else *thr = (long long)c;
+    return TWC_OK;
+}
+
+}  // namespace twc
+
+using namespace twc;
+
+extern "C" {
+
+int32_t twc_version(void) { return 100; }
+
+const char* twc_status_string(twc_status s) {
+    switch (s) {
+        case TWC_OK: return "TWC_OK";
+        case TWC_EINVAL: return "TWC_EINVAL: invalid argument";
+        case TWC_EWORKSPACE: return "TWC_EWORKSPACE: workspace too small or misaligned";
+        case TWC_ECUDA: return "TWC_ECUDA: CUDA error";
+        case TWC_EGRAPH: return "TWC_EGRAPH: CSR violates the input precondition";
+    }
+    return "unknown twc_status";
+}
+
+const char* twc_last_error(void) { return g_err.c_str(); }
+
+size_t twc_score_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes) {
+    (void)rowptr_bytes;
+    if (n < 0 || m < 0) return 0;
+    return score_ws_bytes(n, m);
+}
+
+size_t twc_cluster_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes) {
+    (void)rowptr_bytes;
+    if (n < 0 || m < 0) return 0;
+    return cluster_ws_bytes(n, m);
+}
+
+int64_t twc_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+twc_status twc_score(const twc_csr* g, void* ws, size_t ws_bytes, int32_t* t, int32_t* wedge,
+                     int32_t* tw, void* stream) {
+    return twc_score_ex(g, ws, ws_bytes, t, wedge, tw, stream, nullptr);
+}
+
+twc_status twc_score_ex(const twc_csr* g, void* ws, size_t ws_bytes, int32_t* t, int32_t* wedge,
+                        int32_t* tw, void* stream, void* const* events) {
+    cudaEvent_t* ev = reinterpret_cast<cudaEvent_t*>(const_cast<void**>(events));
+    g_err.clear();
+    twc_status st = check_csr(g);
+    if (st) return st;
+    if (g->m > 0 && (!t || !wedge || !tw)) return fail(TWC_EINVAL, "output array is NULL");
+    if (g->m == 0) {
+        if (ev) {
+            cudaStream_t s0 = static_cast<cudaStream_t>(stream);
+            for (int i = 0; i < 4; ++i) record(ev, i, s0);
+        }
+        return TWC_OK;
+    }
+    st = check_ws(ws, ws_bytes, score_ws_bytes(g->n, g->m));
+    if (st) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (g->rowptr_bytes == 4)
+        e = score_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx, ws,
+                            ws_bytes, t, wedge, tw, s, ev);
+    else
+        e = score_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr), g->colidx,
+                                  ws, ws_bytes, t, wedge, tw, s, ev);
+    return cuda_status(e, "twc_score");
+}
+
+static twc_status sweep_common(const twc_csr* g, const int32_t* tw, const long long* thr, int k,
+                               void* ws, size_t ws_bytes, int32_t* labels, int64_t* stats,
+                               void* stream, cudaEvent_t* ev = nullptr) {
+    if (g->n > 0 && !labels) return fail(TWC_EINVAL, "labels is NULL");
+    if (g->m > 0 && !tw) return fail(TWC_EINVAL, "tw is NULL");
+    twc_status st = check_ws(ws, ws_bytes, cluster_ws_bytes(g->n, g->m));
+    if (st) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (g->rowptr_bytes == 4)
+        e = sweep_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx, tw, thr, k,
+                            ws, ws_bytes, labels, reinterpret_cast<long long*>(stats), s, ev);
+    else
+        e = sweep_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr), g->colidx,
+                                  tw, thr, k, ws, ws_bytes, labels,
+                                  reinterpret_cast<long long*>(stats), s, ev);
+    return cuda_status(e, "twc_cluster/twc_sweep");
+}
+
+twc_status twc_cluster(const twc_csr* g, const int32_t* tw, double delta, void* ws,
+                       size_t ws_bytes, int32_t* labels, int64_t* stats, void* stream) {
+    g_err.clear();
+    twc_status st = check_csr(g);
+    if (st) return st;
+    long long thr;
+    st = delta_to_thr(delta, &thr);
+    if (st) return st;
+    return sweep_common(g, tw, &thr, 1, ws, ws_bytes, labels, stats, stream);
+}
+
+twc_status twc_sweep(const twc_csr* g, const int32_t* tw, const double* deltas_host, int32_t k,
+                     void* ws, size_t ws_bytes, int32_t* labels, int64_t* stats, void* stream) {
+    return twc_sweep_ex(g, tw, deltas_host, k, ws, ws_bytes, labels, stats, stream, nullptr);
+}
+
+twc_status twc_sweep_ex(const twc_csr* g, const int32_t* tw, const double* deltas_host,
+                        int32_t k, void* ws, size_t ws_bytes, int32_t* labels, int64_t* stats,
+                        void* stream, void* const* events) {
+    cudaEvent_t* ev = reinterpret_cast<cudaEvent_t*>(const_cast<void**>(events));
+    g_err.clear();
+    twc_status st = check_csr(g);
+    if (st) return st;
+    if (k < 1 || k > 1024) return fail(TWC_EINVAL, "k=%d must be in [1, 1024]", k);
+    if (!deltas_host) return fail(TWC_EINVAL, "deltas_host is NULL");
+    long long thr[1024];
+    for (int i = 0; i < k; ++i) {
+        st = delta_to_thr(deltas_host[i], &thr[i]);
+        if (st) return st;
+    }
+    return sweep_common(g, tw, thr, k, ws, ws_bytes, labels, stats, stream, ev);
+}
+
+// ---- end-to-end from host buffers --------------------------------------------------------
+struct PipeWs {
+    void* rowptr;
+    int *colidx, *t, *wedge, *tw, *labels;
+    long long* stats;
+    void* inner;
+    size_t inner_bytes;
+};
+
+static PipeWs carve_pipe(Carver& cv, int64_t n, int64_t m, int rb, int k) {
+    PipeWs w;
+    w.rowptr = cv.take<char>((size_t)(n + 1) * rb);
+    w.colidx = cv.take<int>(2 * m);
+    w.t = cv.take<int>(m);
+    w.wedge = cv.take<int>(m);
+    w.tw = cv.take<int>(m);
+    w.labels = cv.take<int>((size_t)k * n);
+    w.stats = cv.take<long long>(2 * (size_t)k);
+    w.inner_bytes = std::max(score_ws_bytes(n, m), cluster_ws_bytes(n, m));
+    w.inner = cv.take<char>(w.inner_bytes);
+    return w;
+}
+
+size_t twc_pipeline_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes, int32_t k) {
+    if (n < 0 || m < 0 || (rowptr_bytes != 4 && rowptr_bytes != 8) || k < 1) return 0;
+    Carver cv(nullptr, 0);
+    carve_pipe(cv, n, m, rowptr_bytes, k);
+    return cv.used;
+}
+
+twc_status twc_pipeline_host(const twc_csr* gh, const double* deltas_host, int32_t k, void* ws,
+                             size_t ws_bytes, int32_t* t, int32_t* wedge, int32_t* tw,
+                             int32_t* labels, int64_t* stats, void* stream) {
+    g_err.clear();
+    twc_status st = check_csr(gh);
+    if (st) return st;
+    if (k < 1 || k > 1024) return fail(TWC_EINVAL, "k=%d must be in [1, 1024]", k);
+    if (!deltas_host) return fail(TWC_EINVAL, "deltas_host is NULL");
+    long long thr[1024];
+    for (int i = 0; i < k; ++i) {
+        st = delta_to_thr(deltas_host[i], &thr[i]);
+        if (st) return st;
+    }
+    const int64_t n = gh->n, m = gh->m;
+    const int rb = gh->rowptr_bytes;
+    st = check_ws(ws, ws_bytes, twc_pipeline_workspace_bytes(n, m, rb, k));
+    if (st) return st;
+    Carver cv(ws, ws_bytes);
+    PipeWs w = carve_pipe(cv, n, m, rb, k);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaSuccess;
+    if (n > 0) e = cudaMemcpyAsync(w.rowptr, gh->rowptr, (size_t)(n + 1) * rb, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && m > 0)
+        e = cudaMemcpyAsync(w.colidx, gh->colidx, sizeof(int) * 2 * (size_t)m, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "twc_pipeline_host H2D");
+    twc_csr gd = *gh;
+    gd.rowptr = w.rowptr;
+    gd.colidx = w.colidx;
+    if (m > 0) {
+        if (rb == 4)
+            e = score_impl<int>(n, m, static_cast<const int*>(gd.rowptr), gd.colidx, w.inner,
+                                w.inner_bytes, w.t, w.wedge, w.tw, s);
+        else
+            e = score_impl<long long>(n, m, static_cast<const long long*>(gd.rowptr), gd.colidx,
+                                      w.inner, w.inner_bytes, w.t, w.wedge, w.tw, s);
+        if (e != cudaSuccess) return cuda_status(e, "twc_pipeline_host score");
+    }
+    if (rb == 4)
+        e = sweep_impl<int>(n, m, static_cast<const int*>(gd.rowptr), gd.colidx, w.tw, thr, k,
+                            w.inner, w.inner_bytes, w.labels, w.stats, s);
+    else
+        e = sweep_impl<long long>(n, m, static_cast<const long long*>(gd.rowptr), gd.colidx, w.tw,
+                                  thr, k, w.inner, w.inner_bytes, w.labels, w.stats, s);
+    if (e != cudaSuccess) return cuda_status(e, "twc_pipeline_host sweep");
+    const size_t mb = sizeof(int) * (size_t)m;
+    if (t && m) e = cudaMemcpyAsync(t, w.t, mb, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && wedge && m) e = cudaMemcpyAsync(wedge, w.wedge, mb, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && tw && m) e = cudaMemcpyAsync(tw, w.tw, mb, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && labels && n)
+        e = cudaMemcpyAsync(labels, w.labels, sizeof(int) * (size_t)k * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && stats)
+        e = cudaMemcpyAsync(stats, w.stats, sizeof(long long) * 2 * (size_t)k, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_status(e, "twc_pipeline_host D2H");
+    return cuda_status(cudaStreamSynchronize(s), "twc_pipeline_host sync");
+}
+
+twc_status twc_validate_csr(const twc_csr* g, int32_t* verdict, void* stream) {
+    g_err.clear();
+    twc_status st = check_csr(g);
+    if (st) return st;
+    if (!verdict) return fail(TWC_EINVAL, "verdict is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (g->rowptr_bytes == 4)
+        e = validate_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx, verdict, s);
+    else
+        e = validate_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr),
+                                     g->colidx, verdict, s);
+    if (e != cudaSuccess) return cuda_status(e, "twc_validate_csr");
+    int h = 0;
+    e = cudaMemcpyAsync(&h, verdict, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, "twc_validate_csr");
+    if (h) return fail(TWC_EGRAPH, "CSR invalid, verdict bits 0x%x", h);
+    return TWC_OK;
+}
+
+}  // extern "C"

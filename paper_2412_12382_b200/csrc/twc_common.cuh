@@ -1,0 +1,90 @@
+// twc_common.cuh -- device helpers shared by the TW kernels (sm_100a).
+//
+// Product code only: nothing here is shared with oracle/ (DESIGN.md "Independence").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace twc {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// Largest index i in [0, len) with a[i] <= x, given a sorted ascending and a[0] <= x.
+template <typename T, typename U>
+__device__ __forceinline__ int last_le(const T* a, int len, U x) {
+    int lo = 0, hi = len;  // invariant: a[lo] <= x, answer in [lo, hi)
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// First index i in [0, len) with a[i] >= x (len if none); a sorted ascending.
+template <typename T>
+__device__ __forceinline__ int lower_bound(const T* a, int len, T x) {
+    int lo = 0, hi = len;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// Branch-light lower bound for short sorted lists (membership probes in smem).
+template <typename T>
+__device__ __forceinline__ int lower_bound_bl(const T* a, int len, T x) {
+    const T* base = a;
+    int n = len;
+    while (n > 1) {
+        int half = n >> 1;
+        base = (base[half - 1] < x) ? base + half : base;
+        n -= half;
+    }
+    return (int)(base - a) + ((n == 1 && *base < x) ? 1 : 0);
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int y = __shfl_up_sync(FULL, v, d);
+        if (lane >= d) v += y;
+    }
+    return v;
+}
+
+template <int W>
+__device__ __forceinline__ int group_sum(int v) {
+#pragma unroll
+    for (int d = W >> 1; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d, W);
+    return v;
+}
+
+__device__ __forceinline__ int warp_max(int v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = max(v, __shfl_xor_sync(FULL, v, d));
+    return v;
+}
+
+__device__ __forceinline__ long long block_sum_ll(long long v, long long* s_tmp /*[32]*/) {
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+    __syncthreads();
+    if (lane == 0) s_tmp[wid] = v;
+    __syncthreads();
+    long long r = 0;
+    if (wid == 0) {
+        r = (lane < (int)(blockDim.x >> 5)) ? s_tmp[lane] : 0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) r += __shfl_xor_sync(FULL, r, d);
+    }
+    return r;  // valid in thread 0
+}
+
+// key(u) = (deg(u), u): u -> v iff key(u) < key(v) (strict total order, reading C9).
+__device__ __forceinline__ bool key_less(int du, int u, int dv, int v) {
+    return du < dv || (du == dv && u < v);
+}
+
+}  // namespace twc

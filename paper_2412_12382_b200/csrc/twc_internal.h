@@ -1,0 +1,69 @@
+// twc_internal.h -- host-side launchers shared between the translation units of libtwc.so.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace twc {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// Bump allocator over a caller-provided workspace (the library never allocates).
+struct Carver {
+    char* base;
+    size_t cap, used = 0;
+    Carver(void* b, size_t c) : base(static_cast<char*>(b)), cap(c) {}
+    template <typename T>
+    T* take(size_t count) {
+        size_t bytes = align_up(count * sizeof(T) + 1);
+        T* p = reinterpret_cast<T*>(base ? base + used : nullptr);
+        used += bytes;
+        return p;
+    }
+    bool ok() const { return used <= cap; }
+};
+
+int num_sms();
+
+// Launch accounting (twc_kernel_launches) and optional phase events (twc_*_ex).
+void count_launches(int k);
+inline void record(cudaEvent_t* ev, int i, cudaStream_t s) {
+    if (ev && ev[i]) cudaEventRecord(ev[i], s);
+}
+
+// ---- scan (twc_scan.cu): out[0] = 0, out[i+1] = in[0] + ... + in[i], for i < len ----------
+size_t scan_temp_bytes(int64_t len);
+void exclusive_scan(const int* in, int* out, int64_t len, int* temp, cudaStream_t s);
+
+// ---- row tiling (twc_scan.cu): trow[i] = row holding item i*tile of offsets off[0..nrows] ---
+constexpr int kTile = 1024;  // canonical edges per tile in the edge-parallel kernels
+__host__ __device__ inline int64_t num_tiles(int64_t total) { return (total + kTile - 1) / kTile; }
+void tile_first_rows(const int* off, int nrows, int64_t total, int* trow, cudaStream_t s);
+
+// ---- canonical edge offsets (twc_scan.cu) ---------------------------------------------------
+// up[u] = #{v in N(u): v > u};  eoff = exclusive scan of up  (S:66-69 canonical order)
+template <typename RP>
+void upper_counts(int64_t n, const RP* rowptr, const int* colidx, int* up, cudaStream_t s);
+
+// ---- score (twc_score.cu) ------------------------------------------------------------------
+size_t score_ws_bytes(int64_t n, int64_t m);
+template <typename RP>
+cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
+                       size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
+                       cudaEvent_t* ev = nullptr);
+
+// ---- cluster (twc_cluster.cu) --------------------------------------------------------------
+size_t cluster_ws_bytes(int64_t n, int64_t m);
+// thresholds already converted to integer "keep iff tw >= thr[i]" form, any order.
+template <typename RP>
+cudaError_t sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, const int* tw,
+                       const long long* thr, int k, void* ws, size_t ws_bytes, int* labels,
+                       long long* stats, cudaStream_t s, cudaEvent_t* ev = nullptr);
+
+// ---- validation (twc_cluster.cu) -----------------------------------------------------------
+template <typename RP>
+cudaError_t validate_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+                          int* verdict, cudaStream_t s);
+
+}  // namespace twc

@@ -1,0 +1,83 @@
+"""CPU-side checks of the C-ABI library: it loads without a GPU, exports every function that
+include/twc.h declares, and rejects bad arguments before touching the device."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2412_12382_b200 as twc
+from paper_2412_12382_b200 import build as twc_build
+
+
+@pytest.fixture(scope="module")
+def lib():
+    twc_build.build()
+    return twc.load_library()
+
+
+def test_exports_every_header_function(lib):
+    names = twc.header_functions()
+    assert len(names) >= 11
+    for name in names:
+        assert hasattr(lib, name), name
+    assert lib.twc_version() == 100
+
+
+def test_status_strings(lib):
+    for s in range(5):
+        assert lib.twc_status_string(s)
+    assert lib.twc_status_string(99) == b"unknown twc_status"
+
+
+def test_workspace_queries_are_host_only(lib):
+    for n, m in [(0, 0), (10, 20), (4_000_000, 35_000_000)]:
+        a = lib.twc_score_workspace_bytes(n, m, 8)
+        b = lib.twc_cluster_workspace_bytes(n, m, 8)
+        c = lib.twc_pipeline_workspace_bytes(n, m, 8, 16)
+        assert a > 0 and b > 0 and c >= a
+    # score workspace ~ 3 n + 2 m int32 + small
+    a = lib.twc_score_workspace_bytes(4_000_000, 35_000_000, 8)
+    assert 4 * (2 * 35_000_000 + 5 * 4_000_000) <= a <= 4 * (2 * 35_000_000 + 5 * 4_000_000) + (1 << 22)
+    assert lib.twc_pipeline_workspace_bytes(10, 10, 3, 1) == 0
+
+
+def _csr(n, m, rb=4, rowptr=1, colidx=2):
+    return twc._Csr(n, m, ctypes.c_void_p(rowptr), rb, ctypes.c_void_p(colidx))
+
+
+def test_argument_errors_before_device(lib):
+    P = ctypes.c_void_p
+    g = _csr(10, 5, rb=3)
+    assert lib.twc_score(ctypes.byref(g), None, 0, P(1), P(1), P(1), None) == twc.TWC_EINVAL
+    assert b"rowptr_bytes" in lib.twc_last_error()
+    g = _csr(-1, 5)
+    assert lib.twc_score(ctypes.byref(g), None, 0, P(1), P(1), P(1), None) == twc.TWC_EINVAL
+    g = _csr(10, 1 << 31, rb=8)
+    assert lib.twc_score(ctypes.byref(g), None, 0, P(1), P(1), P(1), None) == twc.TWC_EINVAL
+    g = _csr(10, 1 << 30, rb=4)          # 2m does not fit int32 rowptr
+    assert lib.twc_score(ctypes.byref(g), None, 0, P(1), P(1), P(1), None) == twc.TWC_EINVAL
+    g = _csr(10, 5)
+    assert lib.twc_score(ctypes.byref(g), None, 0, None, P(1), P(1), None) == twc.TWC_EINVAL
+    assert lib.twc_score(ctypes.byref(g), None, 0, P(1), P(1), P(1), None) == twc.TWC_EWORKSPACE
+    assert lib.twc_score(ctypes.byref(g), P(256), 16, P(1), P(1), P(1), None) == twc.TWC_EWORKSPACE
+    assert lib.twc_score(ctypes.byref(g), P(100), 1 << 30, P(1), P(1), P(1), None) == twc.TWC_EWORKSPACE
+    assert b"aligned" in lib.twc_last_error()
+    assert lib.twc_cluster(ctypes.byref(g), P(1), float("nan"), None, 0, P(1), None, None) == twc.TWC_EINVAL
+    d = (ctypes.c_double * 1)(0.0)
+    assert lib.twc_sweep(ctypes.byref(g), P(1), ctypes.cast(d, P), 0, None, 0, P(1), None, None) == twc.TWC_EINVAL
+    assert lib.twc_sweep(ctypes.byref(g), P(1), None, 1, None, 0, P(1), None, None) == twc.TWC_EINVAL
+    assert lib.twc_validate_csr(ctypes.byref(g), None, None) == twc.TWC_EINVAL
+    assert lib.twc_score(None, None, 0, P(1), P(1), P(1), None) == twc.TWC_EINVAL
+
+
+def test_empty_graph_score_is_ok_without_device(lib):
+    g = _csr(5, 0)
+    assert lib.twc_score(ctypes.byref(g), None, 0, None, None, None, None) == twc.TWC_OK
+
+
+def test_product_package_never_imports_oracle():
+    import pathlib
+    root = pathlib.Path(twc.__file__).parent
+    for p in list(root.rglob("*.py")) + list(root.rglob("*.cu")) + list(root.rglob("*.cuh")) + list(root.rglob("*.h")):
+        txt = p.read_text()
+        assert "import oracle" not in txt and "from oracle" not in txt and "twc_oracle" not in txt, p

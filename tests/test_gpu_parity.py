@@ -1,0 +1,206 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Bar (north_star): t, wedge, TW bit-exact; labels bit-exact (both
+sides emit min-vertex-id labels).  Sizes span many tiles with ragged tails; configs 1-5 run at
+their full BASELINE.json sizes in the launch configuration bench.py times."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import graphgen as gg
+import harness
+import paper_2412_12382_b200 as twc
+from paper_2412_12382_b200 import build as twc_build
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: the gpu tests need a B200 (there is no CPU fallback)")
+    twc_build.build()
+    twc.load_library()
+
+
+def gpu_score(g):
+    rp, ci = harness.to_device(g)
+    t, w, tw = twc.twc_score(rp, ci)
+    torch.cuda.synchronize()
+    return t.cpu().numpy(), w.cpu().numpy(), tw.cpu().numpy()
+
+
+def gpu_sweep(g, tw, deltas):
+    rp, ci = harness.to_device(g)
+    twd = torch.from_numpy(np.ascontiguousarray(tw)).cuda()
+    lab, st = twc.twc_sweep(rp, ci, twd, deltas)
+    torch.cuda.synchronize()
+    return lab.cpu().numpy(), st.cpu().numpy()
+
+
+def assert_score_parity(oracle_mod, g):
+    ot, ow, otw = oracle_mod.score(g)
+    gt, gw, gtw = gpu_score(g)
+    assert gt.shape == ot.shape
+    bad = np.nonzero((gt != ot) | (gw != ow) | (gtw != otw))[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first at {bad[:5]}: gpu t={gt[bad[:5]]} oracle t={ot[bad[:5]]}"
+    return otw
+
+
+def assert_cluster_parity(oracle_mod, g, tw, deltas):
+    lab, st = gpu_sweep(g, tw, deltas)
+    for i, d in enumerate(deltas):
+        ol, kept, ncomp = oracle_mod.cluster(g, tw, d)
+        assert np.array_equal(lab[i], ol), (d, np.nonzero(lab[i] != ol)[0][:5])
+        assert (int(st[i, 0]), int(st[i, 1])) == (kept, ncomp), d
+
+
+# ------------------------------------------------------------------ small / closed forms
+
+@pytest.mark.parametrize("maker", [
+    lambda: gg.complete(3), lambda: gg.complete(60), lambda: gg.path(2), lambda: gg.path(9),
+    lambda: gg.cycle(31), lambda: gg.star(50, 25), lambda: gg.complete_bipartite(5, 9),
+    lambda: gg.wheel(20), lambda: gg.bridge_triangles()])
+def test_small_closed_forms(oracle_mod, maker):
+    g = maker()
+    tw = assert_score_parity(oracle_mod, g)
+    assert_cluster_parity(oracle_mod, g, tw, [-math.inf, -2.0, 0.0, 0.5, math.inf])
+
+
+def test_random_graphs_many_tiles(oracle_mod):
+    rng = np.random.default_rng(11)
+    for it in range(30):
+        n = int(rng.integers(2, 3000))
+        p = float(rng.random()) * min(1.0, 40.0 / n)
+        g = gg.erdos_renyi(n, p, seed=it)
+        tw = assert_score_parity(oracle_mod, g)
+        if tw.size:
+            ds = sorted({float(np.median(tw)), float(tw.min()), float(tw.max()) + 1, -math.inf})
+            assert_cluster_parity(oracle_mod, g, tw, ds)
+
+
+def test_dense_small_many_tiles(oracle_mod):
+    g = gg.erdos_renyi(2000, 0.2, seed=5)          # ~400k edges, d+ up to ~200, ragged tail
+    assert_score_parity(oracle_mod, g)
+
+
+@pytest.mark.parametrize("rb", [np.int32, np.int64])
+def test_hub_closed_forms(rb):
+    """Closed forms, no oracle needed: K_3000 (every d+ beyond the smem staging capacity),
+    star K_{1,200000}, K_{2,100000} (SURVEY 8(c) hub-bin stress)."""
+    g = gg.complete(3000, rb)
+    t, w, tw = gpu_score(g)
+    assert t.size == 3000 * 2999 // 2
+    assert (t == 2998).all() and (w == 0).all() and (tw == 2998).all()
+    g = gg.star(200_000, 7, rb)
+    t, w, tw = gpu_score(g)
+    assert (t == 0).all() and (w == 199_999).all() and (tw == 1 - 200_000).all()
+    g = gg.complete_bipartite(2, 100_000, rb)
+    t, w, tw = gpu_score(g)
+    assert (t == 0).all() and (w == 100_000).all() and (tw == -100_000).all()
+    lab, st = gpu_sweep(g, tw, [-math.inf, -100_000.0, -99_999.5])
+    assert (lab[0] == 0).all() and (lab[1] == 0).all() and np.array_equal(lab[2], np.arange(g.n))
+    assert st.tolist() == [[g.m, 1], [g.m, 1], [0, g.n]]
+
+
+def test_int64_rowptr_small(oracle_mod):
+    for seed in range(5):
+        g = gg.erdos_renyi(700, 0.05, seed).with_rowptr_dtype(np.int64)
+        tw = assert_score_parity(oracle_mod, g)
+        assert_cluster_parity(oracle_mod, g, tw, [float(np.median(tw)), -math.inf])
+
+
+def test_degenerate_inputs():
+    for n in [1, 5]:
+        g = gg.empty(n)
+        rp, ci = harness.to_device(g)
+        t, w, tw = twc.twc_score(rp, ci)
+        assert t.numel() == 0
+        lab, st = twc.twc_cluster(rp, ci, tw, 0.0)
+        assert lab.cpu().tolist() == list(range(n)) and st.cpu().tolist() == [0, n]
+    rp = torch.zeros(1, dtype=torch.int32, device="cuda")   # n = 0
+    ci = torch.zeros(0, dtype=torch.int32, device="cuda")
+    t, w, tw = twc.twc_score(rp, ci)
+    lab, st = twc.twc_cluster(rp, ci, tw, 0.0)
+    assert lab.numel() == 0 and st.cpu().tolist() == [0, 0]
+    g = gg.path(2)                                          # single edge
+    t, w, tw = gpu_score(g)
+    assert (t.tolist(), w.tolist(), tw.tolist()) == ([0], [0], [0])
+    g = gg.csr_from_pairs(10, [0, 5], [1, 9])               # isolated vertices
+    t, w, tw = gpu_score(g)
+    lab, st = gpu_sweep(g, tw, [0.0, 1.0])
+    assert lab[0].tolist() == [0, 0, 2, 3, 4, 5, 6, 7, 8, 5]
+    assert lab[1].tolist() == list(range(10))
+
+
+def test_sweep_equals_independent_clusters_and_duplicates(oracle_mod):
+    g = gg.config_graph(2)
+    _, _, tw = oracle_mod.score(g)
+    rp, ci = harness.to_device(g)
+    twd = torch.from_numpy(tw).cuda()
+    deltas = [-3.0, 0.0, -10.0, -3.0, math.inf, -math.inf, -7.5, 0.0]
+    lab, st = twc.twc_sweep(rp, ci, twd, deltas)
+    for i, d in enumerate(deltas):
+        l1, s1 = twc.twc_cluster(rp, ci, twd, d)
+        assert torch.equal(l1, lab[i]) and torch.equal(s1, st[i]), d
+
+
+def test_determinism_repeated_runs():
+    g = gg.config_graph(3)
+    rp, ci = harness.to_device(g)
+    ref = [x.clone() for x in twc.twc_score(rp, ci)]
+    lab0, _ = twc.twc_sweep(rp, ci, ref[2], harness.SWEEP_GRID)
+    for _ in range(3):
+        out = twc.twc_score(rp, ci)
+        for a, b in zip(ref, out):
+            assert torch.equal(a, b)
+        lab, _ = twc.twc_sweep(rp, ci, ref[2], harness.SWEEP_GRID)
+        assert torch.equal(lab, lab0)
+
+
+def test_pipeline_host_matches_device_path(oracle_mod):
+    g = gg.config_graph(1)
+    ot, ow, otw = oracle_mod.score(g)
+    deltas = harness.thresholds(1, otw)
+    out = twc.twc_pipeline_host(torch.from_numpy(g.rowptr).pin_memory(),
+                                torch.from_numpy(g.colidx).pin_memory(), deltas)
+    assert np.array_equal(out["t"].numpy(), ot)
+    assert np.array_equal(out["wedge"].numpy(), ow)
+    assert np.array_equal(out["tw"].numpy(), otw)
+    for i, d in enumerate(deltas):
+        ol, kept, ncomp = oracle_mod.cluster(g, otw, d)
+        assert np.array_equal(out["labels"][i].numpy(), ol)
+        assert out["stats"][i].tolist() == [kept, ncomp]
+
+
+def test_validate_csr():
+    g = gg.config_graph(1)
+    rp, ci = harness.to_device(g)
+    twc.twc_validate_csr(rp, ci)
+    twc.twc_validate_csr(rp.to(torch.int64), ci)
+    bad = ci.clone()
+    bad[5] = bad[4]                        # duplicate / unsorted entry
+    with pytest.raises(twc.TwcError) as e:
+        twc.twc_validate_csr(rp, bad)
+    assert e.value.status == twc.TWC_EGRAPH
+    h = gg.csr_from_pairs(4, [0, 1], [1, 2])
+    rp, ci = harness.to_device(h)
+    ci2 = ci.clone()
+    ci2[0] = 3                             # 0's neighbour 1 -> 3: asymmetric
+    with pytest.raises(twc.TwcError):
+        twc.twc_validate_csr(rp, ci2)
+    ci3 = ci.clone()
+    ci3[0] = 0                             # self-loop
+    with pytest.raises(twc.TwcError):
+        twc.twc_validate_csr(rp, ci3)
+
+
+# ------------------------------------------------------------------ the five configs, full size
+
+@pytest.mark.parametrize("config", [1, 2, 3, 4, 5])
+def test_config_parity_full_size(oracle_mod, config):
+    oracle_mod.set_threads(oracle_mod.max_threads())
+    g = gg.config_graph(config)
+    tw = assert_score_parity(oracle_mod, g)
+    assert_cluster_parity(oracle_mod, g, tw, harness.thresholds(config, tw))
