@@ -323,12 +323,8 @@ def main_b200(args):
     k3_ms = [sev[i][2].elapsed_time(sev[i][3]) for i in range(K)]
     score_ms = [sev[i][0].elapsed_time(sev[i][3]) for i in range(K)]
     sweep_ms = [wev[i][0].elapsed_time(wev[i][2]) for i in range(K)]
-    total_s = sum(step_ms) / 1000.0
-    if world > 1:
-        tt = torch.tensor([total_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_s = float(tt.item())
-    value = world * m * K / total_s
+    total_s = harness.max_over_ranks(sum(step_ms) / 1000.0, dev)
+    value = harness.weak_scaling_value(m * K, world, total_s)
     ms_per_step = 1000.0 * total_s / K
 
     # ---- roofline of the dominant kernel (K2, oriented intersection), DESIGN.md Sec. 5
@@ -363,13 +359,9 @@ def main_b200(args):
             t0 = time.perf_counter()
             twc.twc_pipeline_host(rp_h, ci_h, deltas, out=out_h, workspace=ws_p, device=dev)
             e_times.append(time.perf_counter() - t0)
-        e_s = sum(e_times) / len(e_times)
-        if world > 1:
-            tt = torch.tensor([e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e_s = float(tt.item())
+        e_s = harness.max_over_ranks(sum(e_times) / len(e_times), dev)
         assert torch.equal(out_h["tw"], tw.cpu()) and torch.equal(out_h["labels"], labels.cpu())
-        e2e = {"value": world * m / e_s, "unit": UNIT,
+        e2e = {"value": harness.weak_scaling_value(m, world, e_s), "unit": UNIT,
                "h2d_bytes_per_step": rp_h.numel() * rp_h.element_size() + ci_h.numel() * 4,
                "d2h_bytes_per_step": 4 * m + 4 * k * n + 16 * k, "ms_per_step": 1000 * e_s}
 

@@ -39,3 +39,24 @@ def to_device(g, device="cuda"):
     rowptr = torch.from_numpy(np.ascontiguousarray(g.rowptr)).to(device)
     colidx = torch.from_numpy(np.ascontiguousarray(g.colidx)).to(device)
     return rowptr, colidx
+
+
+# ------------------------------------------------------------------ multi-rank (bench.py, N > 1)
+def max_over_ranks(value: float, device=None) -> float:
+    """Max of a per-rank float over all ranks (device timings are max-over-ranks, never wall
+    clock); identity when torch.distributed is not initialised."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64,
+                     device=device if device is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def weak_scaling_value(units_per_rank: float, world: int, seconds_max: float) -> float:
+    """Whole-job throughput: every rank processes its own replica of the workload
+    (independent problems, no data-path collective), so units = world x units_per_rank."""
+    return world * units_per_rank / seconds_max
+

@@ -12,8 +12,9 @@
 // racing hooks win (reading C19).
 //
 // Sweep: for thresholds taken in DESCENDING order the kept sets are nested, so one
-// union-find is grown incrementally: step i hooks only the edges with thr_i <= TW < thr_{i-1}
-// and snapshots the compressed labels.
+// union-find is grown incrementally.  One pass buckets every kept edge by the first step that
+// keeps it (its "band": thr_i <= TW < thr_{i-1}); step i then hooks only band i's edges and
+// snapshots the compressed labels.
 #include <algorithm>
 
 #include "twc_common.cuh"
@@ -50,19 +51,72 @@ __global__ void k_init_parent(int64_t n, int* __restrict__ parent) {
     if (u < n) parent[u] = (int)u;
 }
 
-constexpr int kHookThreads = 256;
+constexpr int kSweepThreads = 256;
+constexpr int kItemsPerThread = kTile / kSweepThreads;  // 4
 constexpr int kMaxTileRows = 2048;
+constexpr int kMaxK = 1024;
 
-// Hook every canonical edge with lo <= TW < hi; count edges with TW >= lo into *kept.
+// Band of an edge: the first step (thresholds sorted descending) at which it is kept,
+// b = #{i : thr_sorted[i] > TW}; b == k means kept at no threshold.
+__device__ __forceinline__ int band_of(long long val, const long long* thr, int k) {
+    int lo = 0, hi = k;  // thr descending: predicate thr[i] > val is true on a prefix
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (thr[mid] > val) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// Pass 1: histogram of bands (edges kept at no threshold are not counted).
+__global__ void __launch_bounds__(kSweepThreads) k_band_count(int64_t m, const int* __restrict__ tw,
+                                                              const long long* __restrict__ thr_g,
+                                                              int k, int* __restrict__ cnt) {
+    __shared__ long long s_thr[kMaxK];
+    __shared__ int s_hist[kMaxK];
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        s_thr[i] = thr_g[i];
+        s_hist[i] = 0;
+    }
+    __syncthreads();
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int b = band_of(tw[c], s_thr, k);
+        if (b < k) atomicAdd(&s_hist[b], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += blockDim.x)
+        if (s_hist[i]) atomicAdd(&cnt[i], s_hist[i]);
+}
+
+// Band offsets (exclusive scan, k <= 1024), cursors, and the kept-edge statistics of every
+// threshold (kept(i) = edges in bands 0..i), written at the caller's index order[i].
+__global__ void k_band_offsets(const int* __restrict__ cnt, int k, const int* __restrict__ order,
+                               int* __restrict__ off, int* __restrict__ cursor,
+                               unsigned long long* __restrict__ stats) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int run = 0;
+    for (int i = 0; i < k; ++i) {
+        off[i] = run;
+        cursor[i] = run;
+        run += cnt[i];
+        if (stats) stats[2 * order[i]] = (unsigned long long)run;
+    }
+    off[k] = run;
+}
+
+// Pass 2: scatter each kept edge (u, v) into its band's segment.  Each CTA reserves, per band,
+// one contiguous range per tile (one global atomic per band and tile).
 template <typename RP>
-__global__ void __launch_bounds__(kHookThreads) k_hook_band(
-    int64_t n, int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
+__global__ void __launch_bounds__(kSweepThreads) k_band_scatter(
+    int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int* __restrict__ eoff, const int* __restrict__ trow, const int* __restrict__ tw,
-    long long lo, long long hi, int* __restrict__ parent, unsigned long long* __restrict__ kept) {
+    const long long* __restrict__ thr_g, int k, int* __restrict__ cursor,
+    int2* __restrict__ pairs) {
+    __shared__ long long s_thr[kMaxK];
+    __shared__ int s_cnt[kMaxK];
     __shared__ int s_off[kMaxTileRows + 1];
-    __shared__ long long s_tmp[32];
+    for (int i = threadIdx.x; i < k; i += blockDim.x) s_thr[i] = thr_g[i];
     const int64_t ntiles = num_tiles(m);
-    long long nkept = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int c0 = (int)(tile * kTile);
         const int c1 = (int)min((int64_t)c0 + kTile, m);
@@ -70,13 +124,29 @@ __global__ void __launch_bounds__(kHookThreads) k_hook_band(
         const int nr = trow[tile + 1] - r0 + 1;
         const bool cached = nr <= kMaxTileRows;
         __syncthreads();
+        for (int i = threadIdx.x; i < k; i += blockDim.x) s_cnt[i] = 0;
         if (cached)
             for (int i = threadIdx.x; i <= nr; i += blockDim.x) s_off[i] = eoff[r0 + i];
         __syncthreads();
-        for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
-            const long long val = tw[c];
-            nkept += (val >= lo);
-            if (val >= lo && val < hi) {
+        int band[kItemsPerThread];
+        int rank[kItemsPerThread];
+#pragma unroll
+        for (int it = 0; it < kItemsPerThread; ++it) {
+            const int c = c0 + it * kSweepThreads + threadIdx.x;
+            band[it] = k;
+            if (c < c1) {
+                band[it] = band_of(tw[c], s_thr, k);
+                if (band[it] < k) rank[it] = atomicAdd(&s_cnt[band[it]], 1);
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < k; i += blockDim.x)
+            if (s_cnt[i]) s_cnt[i] = atomicAdd(&cursor[i], s_cnt[i]);
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < kItemsPerThread; ++it) {
+            const int c = c0 + it * kSweepThreads + threadIdx.x;
+            if (c < c1 && band[it] < k) {
                 const int ri = cached ? last_le(s_off, nr + 1, c) : last_le(eoff + r0, nr + 1, c);
                 const int u = r0 + ri;
                 const int eu = cached ? s_off[ri] : eoff[u];
@@ -84,12 +154,22 @@ __global__ void __launch_bounds__(kHookThreads) k_hook_band(
                 const RP rb = rowptr[u];
                 const int du = (int)(rowptr[u + 1] - rb);
                 const int v = colidx[rb + (RP)(du - upu) + (RP)(c - eu)];
-                uf_unite(parent, u, v);
+                pairs[s_cnt[band[it]] + rank[it]] = make_int2(u, v);
             }
         }
     }
-    const long long tot = block_sum_ll(nkept, s_tmp);
-    if (threadIdx.x == 0 && tot) atomicAdd(kept, (unsigned long long)tot);
+}
+
+// Hook the edges of band b (one step of the sweep).
+__global__ void __launch_bounds__(256) k_hook_list(const int2* __restrict__ pairs,
+                                                   const int* __restrict__ off, int b,
+                                                   int* __restrict__ parent) {
+    const int beg = off[b], end = off[b + 1];
+    for (int i = beg + blockIdx.x * blockDim.x + threadIdx.x; i < end;
+         i += gridDim.x * blockDim.x) {
+        const int2 e = pairs[i];
+        uf_unite(parent, e.x, e.y);
+    }
 }
 
 // labels[u] = root(u) (= min id of its component); compress; count roots.
@@ -102,6 +182,7 @@ __global__ void __launch_bounds__(256) k_finalize(int64_t n, int* __restrict__ p
          u += (int64_t)gridDim.x * blockDim.x) {
         const int r = uf_find(parent, (int)u);
         labels[u] = r;
+        parent[u] = r;
         roots += (r == (int)u);
     }
     const long long tot = block_sum_ll(roots, s_tmp);
@@ -109,7 +190,9 @@ __global__ void __launch_bounds__(256) k_finalize(int64_t n, int* __restrict__ p
 }
 
 struct ClusterWs {
-    int *up, *eoff, *scan_tmp, *trow, *parent;
+    int *up, *eoff, *scan_tmp, *trow, *parent, *cnt, *off, *cursor, *order;
+    long long* thr;
+    int2* pairs;
     unsigned long long* stats;  // 2 per threshold (used when caller passes NULL)
 };
 
@@ -120,7 +203,13 @@ static ClusterWs carve_cluster(Carver& cv, int64_t n, int64_t m) {
     w.scan_tmp = cv.take<int>(scan_temp_bytes(n) / sizeof(int));
     w.trow = cv.take<int>(num_tiles(m) + 1);
     w.parent = cv.take<int>(n);
-    w.stats = cv.take<unsigned long long>(2);
+    w.cnt = cv.take<int>(kMaxK + 1);
+    w.off = cv.take<int>(kMaxK + 1);
+    w.cursor = cv.take<int>(kMaxK + 1);
+    w.order = cv.take<int>(kMaxK);
+    w.thr = cv.take<long long>(kMaxK);
+    w.pairs = cv.take<int2>(m);
+    w.stats = cv.take<unsigned long long>(2 * kMaxK);
     return w;
 }
 
@@ -137,20 +226,27 @@ cudaError_t sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     Carver cv(ws, ws_bytes);
     ClusterWs w = carve_cluster(cv, n, m);
     record(ev, 0, s);
-    const int sms = num_sms();
-    if (stats) cudaMemsetAsync(stats, 0, sizeof(long long) * 2 * (size_t)k, s);
+    unsigned long long* st = stats ? reinterpret_cast<unsigned long long*>(stats) : w.stats;
+    cudaMemsetAsync(st, 0, sizeof(long long) * 2 * (size_t)k, s);
     if (n == 0) {
         record(ev, 1, s);
         record(ev, 2, s);
         return cudaGetLastError();
     }
-    // thresholds in descending order (fewest kept edges first)
-    int order[1024];
+    const int sms = num_sms();
+    // thresholds in descending order (fewest kept edges first): kept sets nest
+    int order[kMaxK];
+    long long thr_sorted[kMaxK];
     for (int i = 0; i < k; ++i) order[i] = i;
     for (int i = 1; i < k; ++i)  // insertion sort, k is small
         for (int j = i; j > 0 && thr[order[j]] > thr[order[j - 1]]; --j) {
             int tmp = order[j]; order[j] = order[j - 1]; order[j - 1] = tmp;
         }
+    for (int i = 0; i < k; ++i) thr_sorted[i] = thr[order[i]];
+    // pageable host -> device copies: staged by the driver before the call returns
+    cudaMemcpyAsync(w.thr, thr_sorted, sizeof(long long) * k, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(w.order, order, sizeof(int) * k, cudaMemcpyHostToDevice, s);
+    cudaMemsetAsync(w.cnt, 0, sizeof(int) * (k + 1), s);
     const unsigned nb = (unsigned)((n + 255) / 256);
     k_init_parent<<<nb, 256, 0, s>>>(n, w.parent);
     count_launches(1);
@@ -158,32 +254,28 @@ cudaError_t sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         upper_counts<RP>(n, rowptr, colidx, w.up, s);
         exclusive_scan(w.up, w.eoff, n, w.scan_tmp, s);
         tile_first_rows(w.eoff, (int)n, m, w.trow, s);
+        const int cgrid = (int)std::min<int64_t>((m + kSweepThreads - 1) / kSweepThreads,
+                                                 (int64_t)sms * 8);
+        k_band_count<<<cgrid, kSweepThreads, 0, s>>>(m, tw, w.thr, k, w.cnt);
+        k_band_offsets<<<1, 32, 0, s>>>(w.cnt, k, w.order, w.off, w.cursor, st);
+        const int64_t nt = num_tiles(m);
+        const int sgrid = (int)std::min<int64_t>(nt, (int64_t)sms * 8);
+        k_band_scatter<RP><<<sgrid, kSweepThreads, 0, s>>>(m, rowptr, colidx, w.eoff, w.trow, tw,
+                                                           w.thr, k, w.cursor, w.pairs);
+        count_launches(3);
     }
     record(ev, 1, s);
-    const long long kInf = (long long)1 << 62;
-    long long hi = kInf;
-    const int64_t nt = num_tiles(m);
-    const int hook_grid = (int)std::min<int64_t>(std::max<int64_t>(nt, 1), (int64_t)sms * 8);
+    const int hook_grid = sms * 8;
     const int fin_grid = (int)std::min<int64_t>((int64_t)nb, (int64_t)sms * 8);
     for (int i = 0; i < k; ++i) {
         const int idx = order[i];
-        const long long lo = thr[idx];
-        unsigned long long* st = stats ? reinterpret_cast<unsigned long long*>(stats) + 2 * idx
-                                       : w.stats;
-        if (!stats) cudaMemsetAsync(w.stats, 0, 2 * sizeof(unsigned long long), s);
-        if (m > 0 && lo < hi) {
-            k_hook_band<RP><<<hook_grid, kHookThreads, 0, s>>>(n, m, rowptr, colidx, w.eoff,
-                                                               w.trow, tw, lo, hi, w.parent, st);
-            count_launches(1);
-        } else if (m > 0 && stats && i > 0) {
-            // duplicate threshold: same kept count as the previous (equal) threshold
-            k_hook_band<RP><<<hook_grid, kHookThreads, 0, s>>>(n, m, rowptr, colidx, w.eoff,
-                                                               w.trow, tw, lo, lo, w.parent, st);
+        if (m > 0 && (i == 0 || thr_sorted[i] < thr_sorted[i - 1])) {
+            k_hook_list<<<hook_grid, 256, 0, s>>>(w.pairs, w.off, i, w.parent);
             count_launches(1);
         }
-        k_finalize<<<fin_grid, 256, 0, s>>>(n, w.parent, labels + (size_t)idx * n, st + 1);
+        k_finalize<<<fin_grid, 256, 0, s>>>(n, w.parent, labels + (size_t)idx * n,
+                                            st + 2 * idx + 1);
         count_launches(1);
-        if (lo < hi) hi = lo;
     }
     record(ev, 2, s);
     return cudaGetLastError();

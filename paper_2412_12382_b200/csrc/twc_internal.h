@@ -40,6 +40,9 @@ void exclusive_scan(const int* in, int* out, int64_t len, int* temp, cudaStream_
 constexpr int kTile = 1024;  // canonical edges per tile in the edge-parallel kernels
 __host__ __device__ inline int64_t num_tiles(int64_t total) { return (total + kTile - 1) / kTile; }
 void tile_first_rows(const int* off, int nrows, int64_t total, int* trow, cudaStream_t s);
+// generic: trow[i] = row holding item i*tile of off[0..nrows] (OT = int or long long)
+template <typename OT>
+void tile_rows(const OT* off, int nrows, int64_t total, int tile, int* trow, cudaStream_t s);
 
 // ---- canonical edge offsets (twc_scan.cu) ---------------------------------------------------
 // up[u] = #{v in N(u): v > u};  eoff = exclusive scan of up  (S:66-69 canonical order)

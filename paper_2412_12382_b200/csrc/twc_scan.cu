@@ -105,21 +105,31 @@ void exclusive_scan(const int* in, int* out, int64_t len, int* temp, cudaStream_
     count_launches(3);
 }
 
-__global__ void k_tile_rows(const int* __restrict__ off, int nrows, int64_t total,
+template <typename OT>
+__global__ void k_tile_rows(const OT* __restrict__ off, int nrows, int64_t total, int tile,
                             int64_t ntiles, int* __restrict__ trow) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i > ntiles) return;
-    int64_t item = (i < ntiles) ? i * kTile : total - 1;
-    int r = last_le(off, nrows + 1, (int)item);
+    const OT item = (OT)((i < ntiles) ? i * tile : total - 1);
+    int r = last_le(off, nrows + 1, item);
     trow[i] = min(r, nrows - 1);
 }
 
-void tile_first_rows(const int* off, int nrows, int64_t total, int* trow, cudaStream_t s) {
-    int64_t nt = num_tiles(total);
+template <typename OT>
+void tile_rows(const OT* off, int nrows, int64_t total, int tile, int* trow, cudaStream_t s) {
+    const int64_t nt = (total + tile - 1) / tile;
     if (nt == 0) return;
-    int64_t threads = nt + 1;
-    k_tile_rows<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(off, nrows, total, nt, trow);
+    const int64_t threads = nt + 1;
+    k_tile_rows<OT><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(off, nrows, total, tile, nt,
+                                                                      trow);
     count_launches(1);
+}
+
+template void tile_rows<int>(const int*, int, int64_t, int, int*, cudaStream_t);
+template void tile_rows<long long>(const long long*, int, int64_t, int, int*, cudaStream_t);
+
+void tile_first_rows(const int* off, int nrows, int64_t total, int* trow, cudaStream_t s) {
+    tile_rows<int>(off, nrows, total, kTile, trow, s);
 }
 
 template <typename RP>

@@ -11,6 +11,8 @@
 // The paper's own method (a full-list merge per edge, O(sum d^2) work) is replaced by
 // the oriented count (O(m * arboricity) work); the paper rejected it only for its per-worker
 // count arrays, which one int32 array plus atomics avoids on a GPU.  DESIGN.md Sec. 4.
+#include <climits>
+
 #include "twc_common.cuh"
 #include "twc_internal.h"
 
@@ -23,181 +25,427 @@ __global__ void k0_degrees(int64_t n, const RP* __restrict__ rowptr, int* __rest
     if (u < n) deg[u] = (int)(rowptr[u + 1] - rowptr[u]);
 }
 
-// ------------------------------------------------------- K1a count: up[u], d+[u] per row
-// VW lanes cooperate on one row (VW chosen from the average degree); rows of a warp are
-// consecutive, so the colidx reads of a warp are one contiguous range.
-template <typename RP, int VW>
-__global__ void __launch_bounds__(256) k1_count(int64_t n, const RP* __restrict__ rowptr,
-                                                const int* __restrict__ colidx,
-                                                const int* __restrict__ deg,
-                                                int* __restrict__ up, int* __restrict__ dplus) {
-    constexpr int RPW = 32 / VW;
-    const int lane = threadIdx.x & 31, g = lane / VW, gl = lane % VW;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t u0 = warp * RPW; u0 < n; u0 += nwarps * RPW) {
-        const int64_t u = u0 + g;
-        const bool valid = u < n;
-        const RP beg = valid ? rowptr[u] : 0;
-        const int d = valid ? (int)(rowptr[u + 1] - beg) : 0;
-        const int dmax = warp_max(d);
-        int lower = 0, out = 0;
-        for (int k = gl; k < dmax; k += VW) {
-            if (k < d) {
-                const int v = colidx[beg + k];
-                lower += (v < (int)u);
-                out += key_less(d, (int)u, deg[v], v);
+// ------------------------------------------------ K1: orientation over full-CSR slot tiles
+// The 2m CSR slots are cut into tiles of kSlotTile consecutive slots (rows stay in order, so a
+// tile is a run of whole rows plus partial rows at its ends).  Each CTA caches the tile's row
+// offsets in smem and maps a slot to its row by binary search; each thread takes kSlotItems
+// slots strided by the block size (coalesced colidx reads).
+//   K1a: out-bit per slot (key(u) < key(v)), and per-row counts of upper entries (v > u) and
+//        out-entries, aggregated per row segment inside each warp (ballot + popc) and added to
+//        the row totals with one atomic per segment;  lastcnt[tile] = out-entries of the
+//        tile's last row inside the tile.
+//   carry: out-entries of a tile's first row that lie in earlier tiles.
+//   K1b: scatter: the out-entry at slot p of row u goes to rp_or[u] + (out-entries of row u
+//        before p) -- filtering a sorted row keeps it sorted; for aligned edges (u < v, i.e.
+//        an upper slot) it also records c2o[canonical id] = oriented slot.
+constexpr int kSlotThreads = 256;
+constexpr int kSlotItems = 8;
+constexpr int kSlotTile = kSlotThreads * kSlotItems;  // 2048 slots
+constexpr int kSlotWords = kSlotTile / 32;
+constexpr int kMaxSlotRows = 2048;
+
+template <typename RP>
+struct SlotTile {
+    RP p0, p1;      // [p0, p1) slots of the tile
+    int r0, nr;     // rows r0 .. r0+nr-1 may hold slots of the tile
+    bool cached;    // offsets rowptr[r0 .. r0+nr] cached in smem
+};
+
+template <typename RP>
+__device__ __forceinline__ SlotTile<RP> load_slot_tile(int64_t tile, int64_t m2,
+                                                       const RP* __restrict__ rowptr,
+                                                       const int* __restrict__ ftrow, RP* s_rp) {
+    SlotTile<RP> T;
+    T.p0 = (RP)(tile * kSlotTile);
+    T.p1 = (RP)min((int64_t)T.p0 + kSlotTile, m2);
+    T.r0 = ftrow[tile];
+    T.nr = ftrow[tile + 1] - T.r0 + 1;
+    T.cached = T.nr <= kMaxSlotRows;
+    if (T.cached)
+        for (int i = threadIdx.x; i <= T.nr; i += blockDim.x) s_rp[i] = rowptr[T.r0 + i];
+    return T;
+}
+
+template <typename RP>
+__device__ __forceinline__ int slot_row(const SlotTile<RP>& T, const RP* s_rp,
+                                        const RP* __restrict__ rowptr, RP p) {
+    return T.cached ? last_le(s_rp, T.nr + 1, p) : last_le(rowptr + T.r0, T.nr + 1, p);
+}
+
+template <typename RP>
+__device__ __forceinline__ RP row_off(const SlotTile<RP>& T, const RP* s_rp,
+                                      const RP* __restrict__ rowptr, int ri) {
+    return T.cached ? s_rp[ri] : rowptr[T.r0 + ri];
+}
+
+// Per-warp segmented popcount: lanes hold consecutive slots with non-decreasing row index ri
+// (-1 = invalid lane); returns, in the first lane of each row segment, popc(word & segment).
+__device__ __forceinline__ unsigned segment_mask(int ri, int lane, bool& head) {
+    const int prev = __shfl_up_sync(FULL, ri, 1);
+    head = ri >= 0 && (lane == 0 || prev != ri);
+    const unsigned heads = __ballot_sync(FULL, head) | __ballot_sync(FULL, ri < 0);
+    const unsigned above = heads & ~((2u << lane) - 1u);
+    const int end = above ? __ffs(above) - 1 : 32;
+    const unsigned upto = end == 32 ? FULL : ((1u << end) - 1u);
+    return upto & ~((1u << lane) - 1u);
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(kSlotThreads) k1_count(
+    int64_t m2, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
+    const int* __restrict__ deg, const int* __restrict__ ftrow, int* __restrict__ up,
+    int* __restrict__ dplus, unsigned* __restrict__ outbits, int* __restrict__ lastcnt) {
+    __shared__ RP s_rp[kMaxSlotRows + 1];
+    __shared__ int s_up[kMaxSlotRows];
+    __shared__ int s_out[kMaxSlotRows];
+    const int lane = threadIdx.x & 31;
+    const int64_t ntiles = (m2 + kSlotTile - 1) / kSlotTile;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();
+        const SlotTile<RP> T = load_slot_tile(tile, m2, rowptr, ftrow, s_rp);
+        if (T.cached)
+            for (int i = threadIdx.x; i < T.nr; i += blockDim.x) { s_up[i] = 0; s_out[i] = 0; }
+        __syncthreads();
+#pragma unroll 2
+        for (int it = 0; it < kSlotItems; ++it) {
+            const RP p = T.p0 + (RP)(it * kSlotThreads + threadIdx.x);
+            const bool valid = p < T.p1;
+            int ri = -1;
+            bool out = false, upper = false;
+            if (valid) {
+                ri = slot_row(T, s_rp, rowptr, p);
+                const RP rb = row_off(T, s_rp, rowptr, ri);
+                const int du = (int)(row_off(T, s_rp, rowptr, ri + 1) - rb);
+                const int u = T.r0 + ri;
+                const int v = colidx[p];
+                out = key_less(du, u, deg[v], v);
+                upper = v > u;
+            }
+            const unsigned ow = __ballot_sync(FULL, out);
+            const unsigned uw = __ballot_sync(FULL, upper);
+            if (lane == 0 && T.p0 + (RP)(it * kSlotThreads + (threadIdx.x & ~31)) < T.p1)
+                outbits[(T.p0 + (RP)(it * kSlotThreads + threadIdx.x)) >> 5] = ow;
+            bool head;
+            const unsigned seg = segment_mask(ri, lane, head);
+            if (head) {
+                const int co = __popc(ow & seg), cu = __popc(uw & seg);
+                if (T.cached) {
+                    if (co) atomicAdd(&s_out[ri], co);
+                    if (cu) atomicAdd(&s_up[ri], cu);
+                } else {
+                    if (co) atomicAdd(&dplus[T.r0 + ri], co);
+                    if (cu) atomicAdd(&up[T.r0 + ri], cu);
+                }
             }
         }
-        lower = group_sum<VW>(lower);
-        out = group_sum<VW>(out);
-        if (valid && gl == 0) {
-            up[u] = d - lower;
-            dplus[u] = out;
+        __syncthreads();
+        if (T.cached) {
+            for (int i = threadIdx.x; i < T.nr; i += blockDim.x) {
+                if (s_out[i]) atomicAdd(&dplus[T.r0 + i], s_out[i]);
+                if (s_up[i]) atomicAdd(&up[T.r0 + i], s_up[i]);
+            }
+        }
+        if (threadIdx.x == 0) {
+            const int rl = slot_row(T, s_rp, rowptr, T.p1 - 1);
+            int c = 0;
+            if (T.cached) c = s_out[rl];
+            else {  // uncached tile: recount the last row's out-bits inside the tile
+                const RP rb = row_off(T, s_rp, rowptr, rl);
+                const RP from = rb > T.p0 ? rb : T.p0;
+                for (RP q = from; q < T.p1; ++q) c += (outbits[q >> 5] >> (q & 31)) & 1u;
+            }
+            lastcnt[tile] = c;
         }
     }
 }
 
-// ------------------------------------------- K1b scatter: oriented CSR, rows stay sorted
-template <typename RP, int VW>
-__global__ void __launch_bounds__(256) k1_scatter(int64_t n, const RP* __restrict__ rowptr,
-                                                  const int* __restrict__ colidx,
-                                                  const int* __restrict__ deg,
-                                                  const int* __restrict__ rp_or,
-                                                  int* __restrict__ col_or) {
-    constexpr int RPW = 32 / VW;
-    const int lane = threadIdx.x & 31, g = lane / VW, gl = lane % VW;
-    const unsigned below = (1u << gl) - 1u;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t u0 = warp * RPW; u0 < n; u0 += nwarps * RPW) {
-        const int64_t u = u0 + g;
-        const bool valid = u < n;
-        const RP beg = valid ? rowptr[u] : 0;
-        const int d = valid ? (int)(rowptr[u + 1] - beg) : 0;
-        const int base = valid ? rp_or[u] : 0;
-        const int dmax = warp_max(d);
-        int run = 0;
-        for (int k0 = 0; k0 < dmax; k0 += VW) {
-            const int k = k0 + gl;
-            bool pred = false;
-            int v = 0;
-            if (k < d) {
-                v = colidx[beg + k];
-                pred = key_less(d, (int)u, deg[v], v);
+// carry[t] = out-entries of tile t's first row that lie in tiles before t.
+template <typename RP>
+__global__ void k1_carry(int64_t ntiles, const RP* __restrict__ rowptr,
+                         const int* __restrict__ ftrow, const int* __restrict__ lastcnt,
+                         int* __restrict__ carry) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    const int r0 = ftrow[t];
+    const RP rs = rowptr[r0];
+    int c = 0;
+    for (int64_t q = t - 1; q >= 0 && rs < (RP)((q + 1) * kSlotTile); --q) {
+        c += lastcnt[q];            // row r0 holds the last slot of tile q
+        if (rs >= (RP)(q * kSlotTile)) break;  // row r0 starts inside tile q
+    }
+    carry[t] = c;
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(kSlotThreads) k1_scatter(
+    int64_t m2, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
+    const int* __restrict__ ftrow, const unsigned* __restrict__ outbits,
+    const int* __restrict__ carry, const int* __restrict__ rp_or, const int* __restrict__ eoff,
+    int* __restrict__ col_or, int* __restrict__ c2o) {
+    __shared__ RP s_rp[kMaxSlotRows + 1];
+    __shared__ unsigned s_w[kSlotWords];
+    __shared__ int s_wpre[kSlotWords + 1];
+    const int64_t ntiles = (m2 + kSlotTile - 1) / kSlotTile;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();
+        const SlotTile<RP> T = load_slot_tile(tile, m2, rowptr, ftrow, s_rp);
+        const int nw = (int)((T.p1 - T.p0 + 31) >> 5);
+        if (threadIdx.x < 32) {  // word prefix of the tile's out-bits (64 words, one warp)
+            const int lane = threadIdx.x;
+            const unsigned a = lane < nw ? outbits[(T.p0 >> 5) + lane] : 0u;
+            const unsigned b = lane + 32 < nw ? outbits[(T.p0 >> 5) + lane + 32] : 0u;
+            s_w[lane] = a;
+            s_w[lane + 32] = b;
+            const int ia = warp_incl_scan(__popc(a), lane);
+            const int ta = __shfl_sync(FULL, ia, 31);
+            const int ib = warp_incl_scan(__popc(b), lane);
+            s_wpre[lane] = ia - __popc(a);
+            s_wpre[lane + 32] = ta + ib - __popc(b);
+            if (lane == 31) s_wpre[64] = ta + ib;
+        }
+        __syncthreads();
+        const int cin = carry[tile];
+#pragma unroll 2
+        for (int it = 0; it < kSlotItems; ++it) {
+            const int off = it * kSlotThreads + threadIdx.x;
+            const RP p = T.p0 + (RP)off;
+            if (p >= T.p1) continue;
+            if (!((s_w[off >> 5] >> (off & 31)) & 1u)) continue;
+            const int ri = slot_row(T, s_rp, rowptr, p);
+            const RP rb = row_off(T, s_rp, rowptr, ri);
+            const int u = T.r0 + ri;
+            const int from = rb > T.p0 ? (int)(rb - T.p0) : 0;
+            // out-entries of row u in [from, off) of this tile
+            const int pb_off = s_wpre[off >> 5] + __popc(s_w[off >> 5] & ((1u << (off & 31)) - 1u));
+            const int pb_from = s_wpre[from >> 5] + __popc(s_w[from >> 5] & ((1u << (from & 31)) - 1u));
+            const int rank = pb_off - pb_from + (rb < T.p0 ? cin : 0);
+            const int sl = rp_or[u] + rank;
+            const int v = colidx[p];
+            col_or[sl] = v;
+            if (v > u) {  // aligned edge: canonical id of the upper slot p
+                const int eu = eoff[u];
+                const int du = (int)(row_off(T, s_rp, rowptr, ri + 1) - rb);
+                const int lo = du - (eoff[u + 1] - eu);
+                c2o[eu + (int)(p - rb) - lo] = sl;
             }
-            const unsigned bal = __ballot_sync(FULL, pred);
-            const unsigned gm = (VW == 32) ? bal : ((bal >> (g * VW)) & ((1u << VW) - 1u));
-            if (pred) col_or[base + run + __popc(gm & below)] = v;
-            run += __popc(gm);
         }
     }
 }
 
 // ---------------------------------------------------------- K2 oriented intersection
-// One warp per pivot u (dynamic, chunked work queue).  N+(u) is staged in shared memory (up
-// to kCap entries; longer lists are probed in place in global memory).  The warp flattens
-// the work items {(v, w): v in N+(u), w in N+(v)} so consecutive lanes read consecutive
-// entries of N+(v) (coalesced), and tests w in N+(u) by binary search.  A hit at
-// N+(u)[q] is the triangle {u, v, w}:  t(u,w) and t(u,v) are accumulated in per-warp smem
-// counters (flushed once per pivot), t(v,w) takes one global reduction.
+// Every triangle {u, v, w} is found exactly once, from its lowest-key vertex u (the pivot):
+// v in N+(u), w in N+(v) and w in N+(u).  Work items are the pairs (slot u->v, w in N+(v));
+// there are S = sum_v d-(v) d+(v) of them, and only T (the triangle count) of them hit.
+//
+// Warp-level scheme (persistent grid, chunked atomic pivot queue):
+//  * a warp groups consecutive pivots whose oriented lists total <= kGroupSlots slots and
+//    stages those lists (one contiguous range [A, B) of col_or) in shared memory, together
+//    with a kFilterBits-bit hash filter of their entries; a single pivot with a longer list is
+//    processed in place from global memory (no filter);
+//  * the group's slots are taken 32 at a time (one per lane); each slot u->v contributes
+//    d+(v) items if d+(u) >= 2.  The items of the 32 slots are flattened across the lanes
+//    (exclusive scan of the weights; the segment owning each item is found with one
+//    __reduce_or_sync bit mask + one smem lookup), so consecutive lanes read consecutive
+//    entries of N+(v) (coalesced) whatever the list lengths;
+//  * an item whose w misses the filter cannot be in N+(u) (the common case); the others are
+//    compacted into a per-warp candidate queue and verified 32 at a time by binary search in
+//    the staged sorted list N+(u), so the search runs on full warps;
+//  * a verified hit adds 1 to t(u,w) and t(u,v) in per-warp smem counters (flushed once per
+//    group) and 1 to t(v,w) with one global reduction.
 constexpr int kK2Warps = 8;
-constexpr int kCap = 512;
+constexpr int kGroupSlots = 256;
+constexpr int kFilterBits = 4096;
+constexpr int kFilterWords = kFilterBits / 32;
 constexpr int kPivotChunk = 32;
+constexpr int kCandCap = 64;
+
+struct K2WarpSmem {
+    int list[kGroupSlots];      // staged col_or[A, B)
+    int cnt[kGroupSlots];       // t(u,v)/t(u,w) counters for slots [A, B)
+    unsigned filt[kFilterWords];
+    int prp[33];                // group pivot offsets rp_or[u0 .. u0+np]
+    int pre[32];                // per-lane exclusive prefix of item weights
+    int vst[32];                // start of N+(v) for the lane's slot
+    int plo[32];                // [plo, phi): oriented list of the lane's pivot (absolute slots)
+    int phi[32];
+    int owner[32];              // item-segment owner lookup
+    int cw[kCandCap];           // candidate queue: w, slot of (v,w), owning lane
+    int csv[kCandCap];
+    unsigned char cjj[kCandCap];
+};
+
+__device__ __forceinline__ unsigned filter_hash(int w) {
+    return ((unsigned)w * 2654435761u) >> (32 - 12);  // 12 bits = kFilterBits
+}
+
+// Verify up to 32 queued candidates (lane i takes entry i) and record the hits.
+__device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int ncand, bool staged, int A,
+                                          int r0, const int* __restrict__ col_or,
+                                          int* __restrict__ t_or) {
+    if (lane < ncand) {
+        const int w = S.cw[lane];
+        const int sv = S.csv[lane];
+        const int jj = S.cjj[lane];
+        const int plo = S.plo[jj], len = S.phi[jj] - plo;
+        if (staged) {
+            const int* L = S.list + (plo - A);
+            const int q = lower_bound_bl(L, len, w);
+            if (q < len && L[q] == w) {
+                atomicAdd(&S.cnt[plo - A + q], 1);  // t(u, w)
+                atomicAdd(&S.cnt[r0 + jj - A], 1);  // t(u, v)
+                atomicAdd(&t_or[sv], 1);            // t(v, w)
+            }
+        } else {
+            const int* L = col_or + plo;
+            const int q = lower_bound(L, len, w);
+            if (q < len && L[q] == w) {
+                atomicAdd(&t_or[plo + q], 1);
+                atomicAdd(&t_or[r0 + jj], 1);
+                atomicAdd(&t_or[sv], 1);
+            }
+        }
+    }
+}
 
 __global__ void __launch_bounds__(kK2Warps * 32) k2_intersect(int64_t n,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
                                                               int* __restrict__ t_or,
                                                               int* __restrict__ work) {
-    __shared__ int s_list[kK2Warps][kCap];
-    __shared__ int s_cnt[kK2Warps][kCap];
-    __shared__ int s_pre[kK2Warps][33];
-    __shared__ int s_vst[kK2Warps][32];
+    __shared__ K2WarpSmem smem[kK2Warps];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int* list_s = s_list[wid];
-    int* cnt_s = s_cnt[wid];
-    int* pre = s_pre[wid];
-    int* vst = s_vst[wid];
+    const unsigned lt_mask = (1u << lane) - 1u;
+    K2WarpSmem& S = smem[wid];
     for (;;) {
         int base = 0;
         if (lane == 0) base = atomicAdd(work, kPivotChunk);
         base = __shfl_sync(FULL, base, 0);
         if (base >= n) break;
-        const int uend = (int)min((int64_t)base + kPivotChunk, n);
-        for (int u = base; u < uend; ++u) {
-            const int a = rp_or[u];
-            const int du = rp_or[u + 1] - a;
-            if (du < 2) continue;  // a pivot needs two out-neighbours
-            const bool in_smem = du <= kCap;
-            if (in_smem) {
-                for (int j = lane; j < du; j += 32) {
-                    list_s[j] = col_or[a + j];
-                    cnt_s[j] = 0;
+        const int gend = (int)min((int64_t)base + kPivotChunk, n);
+        int u = base;
+        while (u < gend) {
+            // ---- form a group of pivots [u, u+np) with <= kGroupSlots slots
+            const int np_max = min(32, gend - u);
+            const int A = rp_or[u];
+            const int e_l = (lane < np_max) ? rp_or[u + lane + 1] : INT_MAX;
+            const unsigned fit = __ballot_sync(FULL, lane < np_max && e_l - A <= kGroupSlots);
+            const bool staged = fit != 0u;
+            const int np = staged ? __popc(fit) : 1;
+            const int B = __shfl_sync(FULL, e_l, np - 1);
+            if (lane == 0) S.prp[0] = A;
+            if (lane < np) S.prp[lane + 1] = e_l;
+            if (staged) {
+                for (int i = lane; i < kFilterWords; i += 32) S.filt[i] = 0u;
+                __syncwarp();
+                for (int i = lane; i < B - A; i += 32) {
+                    const int x = col_or[A + i];
+                    S.list[i] = x;
+                    S.cnt[i] = 0;
+                    const unsigned h = filter_hash(x);
+                    atomicOr(&S.filt[h >> 5], 1u << (h & 31));
                 }
             }
             __syncwarp();
-            const int* list = in_smem ? list_s : col_or + a;
-            const int lmin = list[0], lmax = list[du - 1];
-            for (int j0 = 0; j0 < du; j0 += 32) {
-                const int j = j0 + lane;
-                int vs = 0, vd = 0;
-                if (j < du) {
-                    const int v = list[j];
-                    vs = rp_or[v];
-                    vd = rp_or[v + 1] - vs;
-                }
-                const int incl = warp_incl_scan(vd, lane);
-                const int total = __shfl_sync(FULL, incl, 31);
-                pre[lane] = incl - vd;
-                vst[lane] = vs;
-                __syncwarp();
-                for (int k0 = 0; k0 < total; k0 += 32) {
-                    const int k = k0 + lane;
-                    if (k < total) {
-                        const int jj = last_le(pre, 32, k);
-                        const int sv = vst[jj] + (k - pre[jj]);  // oriented slot of v -> w
-                        const int w = col_or[sv];
-                        if (w >= lmin && w <= lmax) {
-                            const int q = lower_bound_bl(list, du, w);
-                            if (list[q] == w) {
-                                if (in_smem) {
-                                    atomicAdd(&cnt_s[q], 1);
-                                    atomicAdd(&cnt_s[j0 + jj], 1);
-                                } else {
-                                    atomicAdd(&t_or[a + q], 1);
-                                    atomicAdd(&t_or[a + j0 + jj], 1);
-                                }
-                                atomicAdd(&t_or[sv], 1);
-                            }
-                        }
+            // ---- rounds of 32 slots
+            for (int r0 = A; r0 < B; r0 += 32) {
+                const int s = r0 + lane;
+                int wt = 0, vs = 0, lo = 0, hi = 0;
+                if (s < B) {
+                    const int v = staged ? S.list[s - A] : col_or[s];
+                    const int pi = staged ? last_le(S.prp, np + 1, s) : 0;
+                    lo = S.prp[pi];
+                    hi = S.prp[pi + 1];
+                    if (hi - lo >= 2) {
+                        vs = rp_or[v];
+                        wt = rp_or[v + 1] - vs;
                     }
                 }
+                const int incl = warp_incl_scan(wt, lane);
+                const int total = __shfl_sync(FULL, incl, 31);
+                const int pre = incl - wt;
+                S.pre[lane] = pre;
+                S.vst[lane] = vs;
+                S.plo[lane] = lo;
+                S.phi[lane] = hi;
+                const unsigned nz = __ballot_sync(FULL, wt > 0);
+                int cur = nz ? __ffs(nz) - 1 : 0;
+                int ncand = 0;
+                __syncwarp();
+                for (int k0 = 0; k0 < total; k0 += 32) {
+                    const bool starts = wt > 0 && pre >= k0 && pre < k0 + 32;
+                    if (starts) S.owner[pre - k0] = lane;
+                    const unsigned bits =
+                        __reduce_or_sync(FULL, starts ? (1u << (pre - k0)) : 0u);
+                    __syncwarp();
+                    const unsigned mine = bits & ((2u << lane) - 1u);
+                    const int jj = mine ? S.owner[31 - __clz(mine)] : cur;
+                    const int k = k0 + lane;
+                    bool cand = false;
+                    int w = 0, sv = 0;
+                    if (k < total) {
+                        sv = S.vst[jj] + (k - S.pre[jj]);  // slot of v -> w
+                        w = col_or[sv];
+                        if (staged) {
+                            const unsigned h = filter_hash(w);
+                            cand = (S.filt[h >> 5] >> (h & 31)) & 1u;
+                        } else {
+                            cand = true;
+                        }
+                    }
+                    const unsigned cb = __ballot_sync(FULL, cand);
+                    if (cand) {
+                        const int pos = ncand + __popc(cb & lt_mask);
+                        S.cw[pos] = w;
+                        S.csv[pos] = sv;
+                        S.cjj[pos] = (unsigned char)jj;
+                    }
+                    ncand += __popc(cb);
+                    cur = __shfl_sync(FULL, jj, 31);
+                    __syncwarp();
+                    if (ncand >= 32) {
+                        k2_verify(S, lane, 32, staged, A, r0, col_or, t_or);
+                        __syncwarp();
+                        if (lane < ncand - 32) {
+                            S.cw[lane] = S.cw[lane + 32];
+                            S.csv[lane] = S.csv[lane + 32];
+                            S.cjj[lane] = S.cjj[lane + 32];
+                        }
+                        ncand -= 32;
+                        __syncwarp();
+                    }
+                }
+                if (ncand > 0) {
+                    k2_verify(S, lane, ncand, staged, A, r0, col_or, t_or);
+                }
                 __syncwarp();
             }
-            if (in_smem) {
-                for (int j = lane; j < du; j += 32) {
-                    const int c = cnt_s[j];
-                    if (c) atomicAdd(&t_or[a + j], c);
+            if (staged) {
+                for (int i = lane; i < B - A; i += 32) {
+                    const int c = S.cnt[i];
+                    if (c) atomicAdd(&t_or[A + i], c);
                 }
             }
             __syncwarp();
+            u += np;
         }
     }
 }
 
 // ---------------------------------------------------------- K3 fused score epilogue
 // Edge-parallel over canonical ids; each CTA takes tiles of kTile ids, caches the tile's
-// canonical row offsets in smem and maps id -> row by binary search.  The oriented slot of
-// (u,v) is found by binary search in the (short) oriented list of its lower-key endpoint.
+// canonical row offsets in smem and maps id -> row by binary search.  The count t of edge
+// (u,v) sits at its oriented slot: for an aligned edge (key(u) < key(v)) K1b recorded it in
+// c2o; for a reversed one it is found by binary search of u in the (short) list N+(v).
+//   wedge = d_u + d_v - 2t - 2   (|N(u) | N(v)| - |N(u) & N(v)| - 2 for a simple graph)
+//   TW    = t - wedge            (Eq. 2)
 constexpr int kK3Threads = 256;
 constexpr int kMaxTileRows = 2048;
 
 template <typename RP>
 __global__ void __launch_bounds__(kK3Threads) k3_score(
-    int64_t n, int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
+    int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int* __restrict__ deg, const int* __restrict__ eoff, const int* __restrict__ trow,
-    const int* __restrict__ rp_or, const int* __restrict__ col_or,
+    const int* __restrict__ rp_or, const int* __restrict__ col_or, const int* __restrict__ c2o,
     const int* __restrict__ t_or, int* __restrict__ t, int* __restrict__ wedge,
     int* __restrict__ tw) {
     __shared__ int s_off[kMaxTileRows + 1];
@@ -207,25 +455,29 @@ __global__ void __launch_bounds__(kK3Threads) k3_score(
         const int c1 = (int)min((int64_t)c0 + kTile, m);
         const int r0 = trow[tile];
         const int nr = trow[tile + 1] - r0 + 1;  // rows touched by this tile
-        const bool cached = nr + 1 <= kMaxTileRows + 1;
+        const bool cached = nr <= kMaxTileRows;
         __syncthreads();
         if (cached)
             for (int i = threadIdx.x; i <= nr; i += blockDim.x) s_off[i] = eoff[r0 + i];
         __syncthreads();
+#pragma unroll 2
         for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
             const int ri = cached ? last_le(s_off, nr + 1, c) : last_le(eoff + r0, nr + 1, c);
             const int u = r0 + ri;
             const int eu = cached ? s_off[ri] : eoff[u];
             const int upu = (cached ? s_off[ri + 1] : eoff[u + 1]) - eu;
-            const int du = deg[u];
-            const RP p = rowptr[u] + (RP)(du - upu) + (RP)(c - eu);  // upper slot of (u,v)
-            const int v = colidx[p];
+            const RP rb = rowptr[u];
+            const int du = (int)(rowptr[u + 1] - rb);
+            const int v = colidx[rb + (RP)(du - upu) + (RP)(c - eu)];  // upper slot of (u,v)
             const int dv = deg[v];
-            int x = u, y = v;
-            if (!key_less(du, u, dv, v)) { x = v; y = u; }
-            const int ob = rp_or[x];
-            const int s = ob + lower_bound(col_or + ob, rp_or[x + 1] - ob, y);
-            const int tt = t_or[s];
+            int sl;
+            if (key_less(du, u, dv, v)) {
+                sl = c2o[c];
+            } else {
+                const int ob = rp_or[v];
+                sl = ob + lower_bound(col_or + ob, rp_or[v + 1] - ob, u);
+            }
+            const int tt = t_or[sl];
             t[c] = tt;
             wedge[c] = du + dv - 2 * tt - 2;
             tw[c] = 3 * tt - du - dv + 2;
@@ -235,20 +487,28 @@ __global__ void __launch_bounds__(kK3Threads) k3_score(
 
 // ------------------------------------------------------------------------ host side
 struct ScoreWs {
-    int *deg, *up, *eoff, *dplus, *rp_or, *scan_tmp, *trow, *col_or, *t_or, *work;
+    int *deg, *up, *eoff, *dplus, *rp_or, *scan_tmp, *trow, *ftrow, *lastcnt, *carry;
+    unsigned* outbits;
+    int *col_or, *t_or, *c2o, *work;
 };
 
 static ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
     ScoreWs w;
+    const int64_t nst = (2 * m + kSlotTile - 1) / kSlotTile;
     w.deg = cv.take<int>(n);
     w.up = cv.take<int>(n);
-    w.eoff = cv.take<int>(n + 1);
     w.dplus = cv.take<int>(n);
+    w.eoff = cv.take<int>(n + 1);
     w.rp_or = cv.take<int>(n + 1);
     w.scan_tmp = cv.take<int>(scan_temp_bytes(n) / sizeof(int));
     w.trow = cv.take<int>(num_tiles(m) + 1);
+    w.ftrow = cv.take<int>(nst + 1);
+    w.lastcnt = cv.take<int>(nst);
+    w.carry = cv.take<int>(nst);
+    w.outbits = cv.take<unsigned>((2 * m + 31) / 32);
     w.col_or = cv.take<int>(m);
     w.t_or = cv.take<int>(m);
+    w.c2o = cv.take<int>(m);
     w.work = cv.take<int>(1);
     return w;
 }
@@ -266,34 +526,6 @@ static int grid_for(int64_t items, int per_block, int max_blocks) {
     return (int)b;
 }
 
-template <typename RP, int VW>
-static void launch_k1(int64_t n, const RP* rowptr, const int* colidx, const ScoreWs& w,
-                      cudaStream_t s) {
-    const int sms = num_sms();
-    const int rows_per_block = 256 / VW;
-    const int grid = grid_for(n, rows_per_block, sms * 8 * 4);
-    k1_count<RP, VW><<<grid, 256, 0, s>>>(n, rowptr, colidx, w.deg, w.up, w.dplus);
-    count_launches(1);
-}
-
-template <typename RP, int VW>
-static void launch_k1b(int64_t n, const RP* rowptr, const int* colidx, const ScoreWs& w,
-                       cudaStream_t s) {
-    const int sms = num_sms();
-    const int rows_per_block = 256 / VW;
-    const int grid = grid_for(n, rows_per_block, sms * 8 * 4);
-    k1_scatter<RP, VW><<<grid, 256, 0, s>>>(n, rowptr, colidx, w.deg, w.rp_or, w.col_or);
-    count_launches(1);
-}
-
-static int pick_vw(int64_t n, int64_t m) {
-    const double avg = n > 0 ? 2.0 * (double)m / (double)n : 0.0;
-    if (avg <= 6) return 4;
-    if (avg <= 12) return 8;
-    if (avg <= 24) return 16;
-    return 32;
-}
-
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
@@ -302,26 +534,30 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     Carver cv(ws, ws_bytes);
     ScoreWs w = carve_score(cv, n, m);
     const int sms = num_sms();
+    const int64_t m2 = 2 * m;
+    const int64_t nst = (m2 + kSlotTile - 1) / kSlotTile;
     record(ev, 0, s);
+    // a1 + a2: degrees, orientation, oriented CSR
+    cudaMemsetAsync(w.up, 0, sizeof(int) * (size_t)n, s);
+    cudaMemsetAsync(w.dplus, 0, sizeof(int) * (size_t)n, s);
     k0_degrees<RP><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rowptr, w.deg);
     count_launches(1);
-    switch (pick_vw(n, m)) {
-        case 4: launch_k1<RP, 4>(n, rowptr, colidx, w, s); break;
-        case 8: launch_k1<RP, 8>(n, rowptr, colidx, w, s); break;
-        case 16: launch_k1<RP, 16>(n, rowptr, colidx, w, s); break;
-        default: launch_k1<RP, 32>(n, rowptr, colidx, w, s); break;
-    }
+    tile_rows<RP>(rowptr, (int)n, m2, kSlotTile, w.ftrow, s);
+    const int sgrid = grid_for(nst, 1, sms * 8);
+    k1_count<RP><<<sgrid, kSlotThreads, 0, s>>>(m2, rowptr, colidx, w.deg, w.ftrow, w.up, w.dplus,
+                                               w.outbits, w.lastcnt);
+    k1_carry<RP><<<(unsigned)((nst + 255) / 256), 256, 0, s>>>(nst, rowptr, w.ftrow, w.lastcnt,
+                                                              w.carry);
+    count_launches(2);
     exclusive_scan(w.up, w.eoff, n, w.scan_tmp, s);
     exclusive_scan(w.dplus, w.rp_or, n, w.scan_tmp, s);
-    switch (pick_vw(n, m)) {
-        case 4: launch_k1b<RP, 4>(n, rowptr, colidx, w, s); break;
-        case 8: launch_k1b<RP, 8>(n, rowptr, colidx, w, s); break;
-        case 16: launch_k1b<RP, 16>(n, rowptr, colidx, w, s); break;
-        default: launch_k1b<RP, 32>(n, rowptr, colidx, w, s); break;
-    }
+    k1_scatter<RP><<<sgrid, kSlotThreads, 0, s>>>(m2, rowptr, colidx, w.ftrow, w.outbits, w.carry,
+                                                 w.rp_or, w.eoff, w.col_or, w.c2o);
+    count_launches(1);
     tile_first_rows(w.eoff, (int)n, m, w.trow, s);
     cudaMemsetAsync(w.t_or, 0, sizeof(int) * (size_t)m, s);
     cudaMemsetAsync(w.work, 0, sizeof(int), s);
+    // a3: oriented intersection
     {
         static int occ = 0;
         if (occ == 0) {
@@ -333,11 +569,12 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         count_launches(1);
         record(ev, 2, s);
     }
+    // a4: canonical gather + wedge + TW
     {
         const int64_t nt = num_tiles(m);
         const int grid = grid_for(nt, 1, sms * 8);
-        k3_score<RP><<<grid, kK3Threads, 0, s>>>(n, m, rowptr, colidx, w.deg, w.eoff, w.trow,
-                                                  w.rp_or, w.col_or, w.t_or, t, wedge, tw);
+        k3_score<RP><<<grid, kK3Threads, 0, s>>>(m, rowptr, colidx, w.deg, w.eoff, w.trow,
+                                                  w.rp_or, w.col_or, w.c2o, w.t_or, t, wedge, tw);
         count_launches(1);
         record(ev, 3, s);
     }

@@ -104,6 +104,22 @@ def test_hub_closed_forms(rb):
     assert st.tolist() == [[g.m, 1], [g.m, 1], [0, g.n]]
 
 
+def test_sparse_rows_uncached_tiles(oracle_mod):
+    """Tiles spanning more rows than the smem row caches hold: a perfect matching on 3 of
+    every 3k ids plus isolated vertices (every tile of canonical ids / CSR slots covers
+    thousands of rows), with a few triangles and a hub mixed in."""
+    k = 40_000
+    a = np.arange(k) * 3
+    hub = 3 * k + 1
+    leaves = np.arange(0, 3 * k, 7)
+    A = np.concatenate([a, [0, 0, 1], np.full(leaves.size, hub)])
+    B = np.concatenate([a + 1, [2, 3, 3], leaves])
+    for rb in (np.int32, np.int64):
+        g = gg.csr_from_pairs(3 * k + 2, A, B, rb)
+        tw = assert_score_parity(oracle_mod, g)
+        assert_cluster_parity(oracle_mod, g, tw, [-math.inf, 0.0, float(np.median(tw))])
+
+
 def test_int64_rowptr_small(oracle_mod):
     for seed in range(5):
         g = gg.erdos_renyi(700, 0.05, seed).with_rowptr_dtype(np.int64)
