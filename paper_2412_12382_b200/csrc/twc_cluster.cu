@@ -105,7 +105,8 @@ __global__ void k_band_offsets(const int* __restrict__ cnt, int k, const int* __
 }
 
 // Pass 2: scatter each kept edge (u, v) into its band's segment.  Each CTA reserves, per band,
-// one contiguous range per tile (one global atomic per band and tile).
+// one contiguous range per tile (one global atomic per band and tile).  A thread handles
+// kItemsPerThread consecutive canonical ids: one row search, then a walk along the rows.
 template <typename RP>
 __global__ void __launch_bounds__(kSweepThreads) k_band_scatter(
     int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
@@ -128,34 +129,50 @@ __global__ void __launch_bounds__(kSweepThreads) k_band_scatter(
         if (cached)
             for (int i = threadIdx.x; i <= nr; i += blockDim.x) s_off[i] = eoff[r0 + i];
         __syncthreads();
+        const int cs = c0 + threadIdx.x * kItemsPerThread;
         int band[kItemsPerThread];
         int rank[kItemsPerThread];
+        bool any = false;
 #pragma unroll
         for (int it = 0; it < kItemsPerThread; ++it) {
-            const int c = c0 + it * kSweepThreads + threadIdx.x;
+            const int c = cs + it;
             band[it] = k;
+            rank[it] = 0;
             if (c < c1) {
                 band[it] = band_of(tw[c], s_thr, k);
-                if (band[it] < k) rank[it] = atomicAdd(&s_cnt[band[it]], 1);
+                if (band[it] < k) {
+                    rank[it] = atomicAdd(&s_cnt[band[it]], 1);
+                    any = true;
+                }
             }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < k; i += blockDim.x)
             if (s_cnt[i]) s_cnt[i] = atomicAdd(&cursor[i], s_cnt[i]);
         __syncthreads();
+        if (!any) continue;
+        int ri = cached ? last_le(s_off, nr + 1, cs) : last_le(eoff + r0, nr + 1, cs);
+        int eu = cached ? s_off[ri] : eoff[r0 + ri];
+        int ee = cached ? s_off[ri + 1] : eoff[r0 + ri + 1];
+        int u = r0 + ri;
+        RP rb = rowptr[u];
+        int du = (int)(rowptr[u + 1] - rb);
 #pragma unroll
         for (int it = 0; it < kItemsPerThread; ++it) {
-            const int c = c0 + it * kSweepThreads + threadIdx.x;
-            if (c < c1 && band[it] < k) {
-                const int ri = cached ? last_le(s_off, nr + 1, c) : last_le(eoff + r0, nr + 1, c);
-                const int u = r0 + ri;
-                const int eu = cached ? s_off[ri] : eoff[u];
-                const int upu = (cached ? s_off[ri + 1] : eoff[u + 1]) - eu;
-                const RP rb = rowptr[u];
-                const int du = (int)(rowptr[u + 1] - rb);
-                const int v = colidx[rb + (RP)(du - upu) + (RP)(c - eu)];
-                pairs[s_cnt[band[it]] + rank[it]] = make_int2(u, v);
+            const int c = cs + it;
+            if (band[it] >= k) continue;
+            if (c >= ee) {
+                do {
+                    ++ri;
+                    eu = ee;
+                    ee = cached ? s_off[ri + 1] : eoff[r0 + ri + 1];
+                } while (c >= ee);
+                u = r0 + ri;
+                rb = rowptr[u];
+                du = (int)(rowptr[u + 1] - rb);
             }
+            const int v = colidx[rb + (RP)(du - (ee - eu)) + (RP)(c - eu)];
+            pairs[s_cnt[band[it]] + rank[it]] = make_int2(u, v);
         }
     }
 }

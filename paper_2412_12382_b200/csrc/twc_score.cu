@@ -106,38 +106,59 @@ __global__ void __launch_bounds__(kSlotThreads) k1_count(
         if (T.cached)
             for (int i = threadIdx.x; i < T.nr; i += blockDim.x) { s_up[i] = 0; s_out[i] = 0; }
         __syncthreads();
-#pragma unroll 2
-        for (int it = 0; it < kSlotItems; ++it) {
-            const RP p = T.p0 + (RP)(it * kSlotThreads + threadIdx.x);
-            const bool valid = p < T.p1;
-            int ri = -1;
-            bool out = false, upper = false;
-            if (valid) {
-                ri = slot_row(T, s_rp, rowptr, p);
-                const RP rb = row_off(T, s_rp, rowptr, ri);
-                const int du = (int)(row_off(T, s_rp, rowptr, ri + 1) - rb);
-                const int u = T.r0 + ri;
-                const int v = colidx[p];
-                out = key_less(du, u, deg[v], v);
-                upper = v > u;
-            }
-            const unsigned ow = __ballot_sync(FULL, out);
-            const unsigned uw = __ballot_sync(FULL, upper);
-            if (lane == 0 && T.p0 + (RP)(it * kSlotThreads + (threadIdx.x & ~31)) < T.p1)
-                outbits[(T.p0 + (RP)(it * kSlotThreads + threadIdx.x)) >> 5] = ow;
-            bool head;
-            const unsigned seg = segment_mask(ri, lane, head);
-            if (head) {
-                const int co = __popc(ow & seg), cu = __popc(uw & seg);
-                if (T.cached) {
-                    if (co) atomicAdd(&s_out[ri], co);
-                    if (cu) atomicAdd(&s_up[ri], cu);
-                } else {
-                    if (co) atomicAdd(&dplus[T.r0 + ri], co);
-                    if (cu) atomicAdd(&up[T.r0 + ri], cu);
+        // this thread: kSlotItems consecutive slots [q0, q0 + kSlotItems)
+        const RP q0 = T.p0 + (RP)(threadIdx.x * kSlotItems);
+        int v[kSlotItems];
+        if (q0 + kSlotItems <= T.p1) {
+            const int4* src = reinterpret_cast<const int4*>(colidx + q0);
+            const int4 a = __ldg(src), b = __ldg(src + 1);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < kSlotItems; ++j) v[j] = (q0 + j < T.p1) ? colidx[q0 + j] : 0;
+        }
+        int dv[kSlotItems];
+#pragma unroll
+        for (int j = 0; j < kSlotItems; ++j) dv[j] = (q0 + j < T.p1) ? deg[v[j]] : 0;
+        unsigned ob = 0;
+        if (q0 < T.p1) {
+            int ri = slot_row(T, s_rp, rowptr, q0);
+            RP rb = row_off(T, s_rp, rowptr, ri), re = row_off(T, s_rp, rowptr, ri + 1);
+            int cu = 0, co = 0;
+#pragma unroll
+            for (int j = 0; j < kSlotItems; ++j) {
+                const RP p = q0 + j;
+                if (p < T.p1) {
+                    if (p >= re) {  // next non-empty row
+                        if (cu || co) {
+                            if (T.cached) { atomicAdd(&s_up[ri], cu); atomicAdd(&s_out[ri], co); }
+                            else { atomicAdd(&up[T.r0 + ri], cu); atomicAdd(&dplus[T.r0 + ri], co); }
+                        }
+                        cu = co = 0;
+                        do {
+                            ++ri;
+                            rb = re;
+                            re = row_off(T, s_rp, rowptr, ri + 1);
+                        } while (p >= re);
+                    }
+                    const int u = T.r0 + ri;
+                    const bool out = key_less((int)(re - rb), u, dv[j], v[j]);
+                    ob |= (unsigned)out << j;
+                    co += out;
+                    cu += v[j] > u;
                 }
             }
+            if (cu || co) {
+                if (T.cached) { atomicAdd(&s_up[ri], cu); atomicAdd(&s_out[ri], co); }
+                else { atomicAdd(&up[T.r0 + ri], cu); atomicAdd(&dplus[T.r0 + ri], co); }
+            }
         }
+        // 4 threads x 8 bits = one 32-bit word of out-bits
+        unsigned word = ob << (8 * (lane & 3));
+        word |= __shfl_xor_sync(FULL, word, 1);
+        word |= __shfl_xor_sync(FULL, word, 2);
+        if ((lane & 3) == 0 && q0 < T.p1) outbits[q0 >> 5] = word;
         __syncthreads();
         if (T.cached) {
             for (int i = threadIdx.x; i < T.nr; i += blockDim.x) {
@@ -148,8 +169,10 @@ __global__ void __launch_bounds__(kSlotThreads) k1_count(
         if (threadIdx.x == 0) {
             const int rl = slot_row(T, s_rp, rowptr, T.p1 - 1);
             int c = 0;
-            if (T.cached) c = s_out[rl];
-            else {  // uncached tile: recount the last row's out-bits inside the tile
+            if (T.cached) {
+                c = s_out[rl];
+            } else {  // uncached tile: recount the last row's out-bits inside the tile
+                __threadfence_block();
                 const RP rb = row_off(T, s_rp, rowptr, rl);
                 const RP from = rb > T.p0 ? rb : T.p0;
                 for (RP q = from; q < T.p1; ++q) c += (outbits[q >> 5] >> (q & 31)) & 1u;
@@ -204,28 +227,43 @@ __global__ void __launch_bounds__(kSlotThreads) k1_scatter(
             if (lane == 31) s_wpre[64] = ta + ib;
         }
         __syncthreads();
+        const int off0 = threadIdx.x * kSlotItems;
+        const RP q0 = T.p0 + (RP)off0;
+        const unsigned bits = (s_w[off0 >> 5] >> (off0 & 31)) & 0xffu;
+        if (q0 >= T.p1 || bits == 0u) continue;
         const int cin = carry[tile];
-#pragma unroll 2
-        for (int it = 0; it < kSlotItems; ++it) {
-            const int off = it * kSlotThreads + threadIdx.x;
-            const RP p = T.p0 + (RP)off;
-            if (p >= T.p1) continue;
-            if (!((s_w[off >> 5] >> (off & 31)) & 1u)) continue;
-            const int ri = slot_row(T, s_rp, rowptr, p);
-            const RP rb = row_off(T, s_rp, rowptr, ri);
-            const int u = T.r0 + ri;
-            const int from = rb > T.p0 ? (int)(rb - T.p0) : 0;
-            // out-entries of row u in [from, off) of this tile
-            const int pb_off = s_wpre[off >> 5] + __popc(s_w[off >> 5] & ((1u << (off & 31)) - 1u));
-            const int pb_from = s_wpre[from >> 5] + __popc(s_w[from >> 5] & ((1u << (from & 31)) - 1u));
-            const int rank = pb_off - pb_from + (rb < T.p0 ? cin : 0);
-            const int sl = rp_or[u] + rank;
+        int ri = slot_row(T, s_rp, rowptr, q0);
+        RP rb = row_off(T, s_rp, rowptr, ri), re = row_off(T, s_rp, rowptr, ri + 1);
+        // out-entries of the current row inside the tile before slot q0
+        int from = rb > T.p0 ? (int)(rb - T.p0) : 0;
+        const int pb0 = s_wpre[off0 >> 5] + __popc(s_w[off0 >> 5] & ((1u << (off0 & 31)) - 1u));
+        int rank = pb0 - (s_wpre[from >> 5] + __popc(s_w[from >> 5] & ((1u << (from & 31)) - 1u))) +
+                   (rb < T.p0 ? cin : 0);
+        int u = T.r0 + ri;
+        int base = rp_or[u];
+#pragma unroll
+        for (int j = 0; j < kSlotItems; ++j) {
+            const RP p = q0 + j;
+            if (!((bits >> j) & 1u)) {
+                continue;
+            }
+            if (p >= re) {  // a new row: its out-entries before p all lie in this thread's run
+                do {
+                    ++ri;
+                    rb = re;
+                    re = row_off(T, s_rp, rowptr, ri + 1);
+                } while (p >= re);
+                u = T.r0 + ri;
+                base = rp_or[u];
+                rank = __popc(bits & ((1u << j) - 1u) & ~((1u << (int)(rb - q0)) - 1u));
+            }
+            const int sl = base + rank;
+            ++rank;
             const int v = colidx[p];
             col_or[sl] = v;
             if (v > u) {  // aligned edge: canonical id of the upper slot p
                 const int eu = eoff[u];
-                const int du = (int)(row_off(T, s_rp, rowptr, ri + 1) - rb);
-                const int lo = du - (eoff[u + 1] - eu);
+                const int lo = (int)(re - rb) - (eoff[u + 1] - eu);
                 c2o[eu + (int)(p - rb) - lo] = sl;
             }
         }
@@ -242,14 +280,14 @@ __global__ void __launch_bounds__(kSlotThreads) k1_scatter(
 //    stages those lists (one contiguous range [A, B) of col_or) in shared memory, together
 //    with a kFilterBits-bit hash filter of their entries; a single pivot with a longer list is
 //    processed in place from global memory (no filter);
-//  * the group's slots are taken 32 at a time (one per lane); each slot u->v contributes
-//    d+(v) items if d+(u) >= 2.  The items of the 32 slots are flattened across the lanes
-//    (exclusive scan of the weights; the segment owning each item is found with one
-//    __reduce_or_sync bit mask + one smem lookup), so consecutive lanes read consecutive
-//    entries of N+(v) (coalesced) whatever the list lengths;
+//  * the group's slots are taken 32 at a time (one per lane); slot u->v owns the items
+//    w in N+(v) if d+(u) >= 2, cut into quads of kQuad consecutive entries.  The quads of the
+//    32 slots are flattened across the lanes (exclusive scan of the quad counts; the segment
+//    owning a quad is found with one __reduce_or_sync bit mask + one smem lookup), so each
+//    lane reads kQuad consecutive entries of one N+(v) and a warp reads a contiguous run;
 //  * an item whose w misses the filter cannot be in N+(u) (the common case); the others are
-//    compacted into a per-warp candidate queue and verified 32 at a time by binary search in
-//    the staged sorted list N+(u), so the search runs on full warps;
+//    appended to a per-warp ring of candidates, verified 32 at a time by binary search in the
+//    staged sorted list N+(u), so the search runs on full warps;
 //  * a verified hit adds 1 to t(u,w) and t(u,v) in per-warp smem counters (flushed once per
 //    group) and 1 to t(v,w) with one global reduction.
 constexpr int kK2Warps = 8;
@@ -257,35 +295,37 @@ constexpr int kGroupSlots = 256;
 constexpr int kFilterBits = 4096;
 constexpr int kFilterWords = kFilterBits / 32;
 constexpr int kPivotChunk = 32;
-constexpr int kCandCap = 64;
+constexpr int kQuad = 4;
+constexpr int kRing = 256;  // >= 31 + 32 * kQuad pending candidates
 
 struct K2WarpSmem {
     int list[kGroupSlots];      // staged col_or[A, B)
     int cnt[kGroupSlots];       // t(u,v)/t(u,w) counters for slots [A, B)
     unsigned filt[kFilterWords];
     int prp[33];                // group pivot offsets rp_or[u0 .. u0+np]
-    int pre[32];                // per-lane exclusive prefix of item weights
+    int pre[32];                // per-lane exclusive prefix of quad counts
     int vst[32];                // start of N+(v) for the lane's slot
+    int vln[32];                // |N+(v)|
     int plo[32];                // [plo, phi): oriented list of the lane's pivot (absolute slots)
     int phi[32];
-    int owner[32];              // item-segment owner lookup
-    int cw[kCandCap];           // candidate queue: w, slot of (v,w), owning lane
-    int csv[kCandCap];
-    unsigned char cjj[kCandCap];
+    int owner[32];              // quad-segment owner lookup
+    int ring[kRing];            // candidates: (owning lane << 16) | index in N+(v)
 };
 
 __device__ __forceinline__ unsigned filter_hash(int w) {
     return ((unsigned)w * 2654435761u) >> (32 - 12);  // 12 bits = kFilterBits
 }
 
-// Verify up to 32 queued candidates (lane i takes entry i) and record the hits.
-__device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int ncand, bool staged, int A,
-                                          int r0, const int* __restrict__ col_or,
+// Verify ring entries [head, head + cnt) (cnt <= 32; lane i takes entry head + i).
+__device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int head, int cnt,
+                                          bool staged, int A, int r0,
+                                          const int* __restrict__ col_or,
                                           int* __restrict__ t_or) {
-    if (lane < ncand) {
-        const int w = S.cw[lane];
-        const int sv = S.csv[lane];
-        const int jj = S.cjj[lane];
+    if (lane < cnt) {
+        const int e = S.ring[(head + lane) & (kRing - 1)];
+        const int jj = e >> 16;
+        const int sv = S.vst[jj] + (e & 0xffff);  // slot of v -> w
+        const int w = col_or[sv];
         const int plo = S.plo[jj], len = S.phi[jj] - plo;
         if (staged) {
             const int* L = S.list + (plo - A);
@@ -307,12 +347,13 @@ __device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int ncand, bo
     }
 }
 
-__global__ void __launch_bounds__(kK2Warps * 32) k2_intersect(int64_t n,
+__global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
                                                               int* __restrict__ t_or,
                                                               int* __restrict__ work) {
-    __shared__ K2WarpSmem smem[kK2Warps];
+    extern __shared__ __align__(16) unsigned char k2_smem_raw[];
+    K2WarpSmem* smem = reinterpret_cast<K2WarpSmem*>(k2_smem_raw);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
     K2WarpSmem& S = smem[wid];
@@ -349,7 +390,7 @@ __global__ void __launch_bounds__(kK2Warps * 32) k2_intersect(int64_t n,
             // ---- rounds of 32 slots
             for (int r0 = A; r0 < B; r0 += 32) {
                 const int s = r0 + lane;
-                int wt = 0, vs = 0, lo = 0, hi = 0;
+                int wt = 0, vs = 0, vd = 0, lo = 0, hi = 0;
                 if (s < B) {
                     const int v = staged ? S.list[s - A] : col_or[s];
                     const int pi = staged ? last_le(S.prp, np + 1, s) : 0;
@@ -357,7 +398,8 @@ __global__ void __launch_bounds__(kK2Warps * 32) k2_intersect(int64_t n,
                     hi = S.prp[pi + 1];
                     if (hi - lo >= 2) {
                         vs = rp_or[v];
-                        wt = rp_or[v + 1] - vs;
+                        vd = rp_or[v + 1] - vs;
+                        wt = (vd + kQuad - 1) / kQuad;
                     }
                 }
                 const int incl = warp_incl_scan(wt, lane);
@@ -365,11 +407,12 @@ __global__ void __launch_bounds__(kK2Warps * 32) k2_intersect(int64_t n,
                 const int pre = incl - wt;
                 S.pre[lane] = pre;
                 S.vst[lane] = vs;
+                S.vln[lane] = vd;
                 S.plo[lane] = lo;
                 S.phi[lane] = hi;
                 const unsigned nz = __ballot_sync(FULL, wt > 0);
                 int cur = nz ? __ffs(nz) - 1 : 0;
-                int ncand = 0;
+                int head = 0, tail = 0;  // candidate ring
                 __syncwarp();
                 for (int k0 = 0; k0 < total; k0 += 32) {
                     const bool starts = wt > 0 && pre >= k0 && pre < k0 + 32;
@@ -380,43 +423,43 @@ __global__ void __launch_bounds__(kK2Warps * 32) k2_intersect(int64_t n,
                     const unsigned mine = bits & ((2u << lane) - 1u);
                     const int jj = mine ? S.owner[31 - __clz(mine)] : cur;
                     const int k = k0 + lane;
-                    bool cand = false;
-                    int w = 0, sv = 0;
+                    int w[kQuad];
+                    int sv0 = 0, nval = 0, i0 = 0;
+                    unsigned cm = 0;
                     if (k < total) {
-                        sv = S.vst[jj] + (k - S.pre[jj]);  // slot of v -> w
-                        w = col_or[sv];
+                        i0 = (k - S.pre[jj]) * kQuad;  // first entry of the quad in N+(v)
+                        sv0 = S.vst[jj] + i0;
+                        nval = min(kQuad, S.vln[jj] - i0);
+#pragma unroll
+                        for (int e = 0; e < kQuad; ++e) w[e] = (e < nval) ? col_or[sv0 + e] : 0;
                         if (staged) {
-                            const unsigned h = filter_hash(w);
-                            cand = (S.filt[h >> 5] >> (h & 31)) & 1u;
+#pragma unroll
+                            for (int e = 0; e < kQuad; ++e) {
+                                const unsigned h = filter_hash(w[e]);
+                                if (e < nval && ((S.filt[h >> 5] >> (h & 31)) & 1u)) cm |= 1u << e;
+                            }
                         } else {
-                            cand = true;
+                            cm = (1u << nval) - 1u;
                         }
                     }
-                    const unsigned cb = __ballot_sync(FULL, cand);
-                    if (cand) {
-                        const int pos = ncand + __popc(cb & lt_mask);
-                        S.cw[pos] = w;
-                        S.csv[pos] = sv;
-                        S.cjj[pos] = (unsigned char)jj;
+                    // append the candidates to the ring as (lane of the slot, index in N+(v))
+                    const int cbase = (jj << 16) | i0;
+#pragma unroll
+                    for (int e = 0; e < kQuad; ++e) {
+                        const bool c = (cm >> e) & 1u;
+                        const unsigned b = __ballot_sync(FULL, c);
+                        if (c) S.ring[(tail + __popc(b & lt_mask)) & (kRing - 1)] = cbase + e;
+                        tail += __popc(b);
                     }
-                    ncand += __popc(cb);
                     cur = __shfl_sync(FULL, jj, 31);
                     __syncwarp();
-                    if (ncand >= 32) {
-                        k2_verify(S, lane, 32, staged, A, r0, col_or, t_or);
-                        __syncwarp();
-                        if (lane < ncand - 32) {
-                            S.cw[lane] = S.cw[lane + 32];
-                            S.csv[lane] = S.csv[lane + 32];
-                            S.cjj[lane] = S.cjj[lane + 32];
-                        }
-                        ncand -= 32;
-                        __syncwarp();
+                    while (tail - head >= 32) {
+                        k2_verify(S, lane, head, 32, staged, A, r0, col_or, t_or);
+                        head += 32;
                     }
+                    __syncwarp();
                 }
-                if (ncand > 0) {
-                    k2_verify(S, lane, ncand, staged, A, r0, col_or, t_or);
-                }
+                if (tail > head) k2_verify(S, lane, head, tail - head, staged, A, r0, col_or, t_or);
                 __syncwarp();
             }
             if (staged) {
@@ -559,13 +602,17 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     cudaMemsetAsync(w.work, 0, sizeof(int), s);
     // a3: oriented intersection
     {
+        const size_t smem = kK2Warps * sizeof(K2WarpSmem);
         static int occ = 0;
         if (occ == 0) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_intersect, kK2Warps * 32, 0);
+            cudaFuncSetAttribute(k2_intersect, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_intersect, kK2Warps * 32, smem);
             if (occ < 1) occ = 1;
         }
         record(ev, 1, s);
-        k2_intersect<<<sms * occ, kK2Warps * 32, 0, s>>>(n, w.rp_or, w.col_or, w.t_or, w.work);
+        k2_intersect<<<sms * occ, kK2Warps * 32, smem, s>>>(n, w.rp_or, w.col_or, w.t_or,
+                                                             w.work);
         count_launches(1);
         record(ev, 2, s);
     }

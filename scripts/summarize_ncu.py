@@ -1,0 +1,116 @@
+#!/usr/bin/env python
+"""Summarise an ncu capture and a launch list into profiles/ (run here, no GPU needed).
+
+    python scripts/summarize_ncu.py TAG gpurun_out/prof_TAG.ncu-rep gpurun_out/launches_TAG.csv
+
+Writes profiles/TAG_ncu_full.md (per-kernel metrics of the --set full capture),
+profiles/TAG_launches.md (per-kernel device time and share of one bench step from the
+--metrics gpu__time_duration.sum launch list; ncu serialises and cold-starts each launch, so
+compare SHARES, not absolute times) and profiles/k2_ncu_summary.json (DRAM bytes per K2
+launch, read by bench.py for roofline.traffic).
+"""
+import csv
+import json
+import os
+import subprocess
+import sys
+from collections import OrderedDict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROF = os.path.join(ROOT, "profiles")
+
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % peak"),
+    ("lts__t_bytes.sum", "L2 bytes"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "threads/inst (of 32)"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("launch__registers_per_thread", "registers"),
+    ("launch__grid_size", "grid"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long_sb"),
+    ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "stall short_sb"),
+    ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier"),
+    ("smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio", "stall math"),
+    ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall wait"),
+]
+
+
+def to_bytes(val, unit):
+    v = float(val.replace(",", ""))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    return v * scale.get(unit, 1)
+
+
+def full_summary(tag, rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    col = {h: i for i, h in enumerate(hdr)}
+    lines = [f"# ncu --set full summary ({tag})", "",
+             "Captured with `ncu --set full --clock-control none --import-source on` on one B200 "
+             "(scripts/gpu_iter.sh); config 5 workload (DC-SBM n=4M, m=35M), one bench step.", ""]
+    k2 = None
+    for r in rows[2:]:
+        name = r[col["Kernel Name"]].split("(")[0].replace("void ", "")
+        lines.append(f"## {name}")
+        lines.append("")
+        lines.append("| metric | value |")
+        lines.append("|---|---|")
+        for key, label in METRICS:
+            if key in col:
+                lines.append(f"| {label} (`{key}`) | {r[col[key]]} {units[col[key]]} |")
+        lines.append("")
+        if "k2_intersect" in name and k2 is None:
+            rd = to_bytes(r[col["dram__bytes_read.sum"]], units[col["dram__bytes_read.sum"]])
+            wr = to_bytes(r[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
+            k2 = {"tag": tag, "dram_bytes_read": rd, "dram_bytes_write": wr,
+                  "dram_bytes_per_launch": rd + wr,
+                  "duration": r[col["gpu__time_duration.sum"]] + " " + units[col["gpu__time_duration.sum"]],
+                  "source": f"profiles/{tag}_ncu_full.md"}
+    with open(os.path.join(PROF, f"{tag}_ncu_full.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    if k2:
+        with open(os.path.join(PROF, "k2_ncu_summary.json"), "w") as f:
+            json.dump(k2, f, indent=1)
+
+
+def launch_summary(tag, path):
+    rows = list(csv.reader(open(path)))
+    i = [k for k, r in enumerate(rows) if r and r[0] == "ID"][0]
+    hdr, data = rows[i], rows[i + 1:]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    seq = [(r[ki].split("(")[0].replace("void ", ""), float(r[vi].replace(",", "")))
+           for r in data if len(r) > vi]
+    idx = [k for k, (nm, _) in enumerate(seq) if "k0_degrees" in nm]
+    last = [x for x in seq[idx[-1]:] if not x[0].startswith("at::")]
+    tot = sum(v for _, v in last)
+    agg, cnt = OrderedDict(), OrderedDict()
+    for nm, v in last:
+        agg[nm] = agg.get(nm, 0.0) + v
+        cnt[nm] = cnt.get(nm, 0) + 1
+    lines = [f"# Launch list of one bench step ({tag})", "",
+             "`ncu --metrics gpu__time_duration.sum --clock-control none` over "
+             "`python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline` (config 5); the "
+             "last complete step.  ncu serialises launches and starts each cold, so the SHARES "
+             "are what compare with bench.py's live phase timings, not the absolute times.", "",
+             "| kernel | launches | device time (us) | share |", "|---|---|---|---|"]
+    for nm, v in agg.items():
+        lines.append(f"| `{nm}` | {cnt[nm]} | {v / 1000:.1f} | {100 * v / tot:.1f}% |")
+    lines.append(f"| **total** | {sum(cnt.values())} | {tot / 1000:.1f} | 100% |")
+    with open(os.path.join(PROF, f"{tag}_launches.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
+if __name__ == "__main__":
+    tag, rep, launches = sys.argv[1], sys.argv[2], sys.argv[3]
+    os.makedirs(PROF, exist_ok=True)
+    full_summary(tag, rep)
+    launch_summary(tag, launches)
+    print("wrote profiles/ for", tag)
