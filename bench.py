@@ -57,7 +57,7 @@ def workload_desc(cfg, g, k):
     c = gg.CONFIGS[cfg]
     kind = "planted-partition SBM" if c["kind"] == "pp" else "degree-corrected SBM"
     return (f"config{cfg}: {kind} n={g.n} m={g.m} (BASELINE.json configs[{cfg - 1}], seed "
-            f"{c['seed']}); step = twc_score + {k}-threshold twc_sweep (filter + CC)")
+            f"{c['seed']}); step = twc_score_sweep: score + {k}-threshold filter + CC sweep, fused")
 
 
 # ----------------------------------------------------------------------------- host stats
@@ -272,6 +272,8 @@ def main_b200(args):
     stream = torch.cuda.current_stream()
     ws_s = torch.empty(twc.twc_score_workspace_bytes(n, m, rb), dtype=torch.uint8, device=dev)
     ws_c = torch.empty(twc.twc_cluster_workspace_bytes(n, m, rb), dtype=torch.uint8, device=dev)
+    ws_f = torch.empty(twc.twc_score_sweep_workspace_bytes(n, m, rb), dtype=torch.uint8,
+                       device=dev)
     t, w, tw = (torch.empty(m, dtype=torch.int32, device=dev) for _ in range(3))
     twc.twc_score(rp, ci, out=(t, w, tw), workspace=ws_s)
     torch.cuda.synchronize()
@@ -287,17 +289,23 @@ def main_b200(args):
             e.record(stream)
         return evs
 
-    def step(se=None, we=None):
+    def step(ev=None):
+        # the whole hot path, fused: score (orient, intersect, epilogue + band binning) + sweep
+        twc.twc_score_sweep(rp, ci, deltas, out=(t, w, tw), labels=labels, stats=stats,
+                            workspace=ws_f, events=ev)
+
+    def step_separate(se=None, we=None):
+        # the same path through the two separate ABI calls
         twc.twc_score(rp, ci, out=(t, w, tw), workspace=ws_s, events=se)
         twc.twc_sweep(rp, ci, tw, deltas, labels=labels, stats=stats, workspace=ws_c, events=we)
 
     for _ in range(args.warmup):
         step()
+        step_separate()
     torch.cuda.synchronize()
 
     K = args.steps
-    sev = [mk(4) for _ in range(K)]
-    wev = [mk(3) for _ in range(K)]
+    fev = [mk(6) for _ in range(K)]
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     torch.cuda.synchronize()
@@ -310,7 +318,7 @@ def main_b200(args):
         for i in range(K):
             flush.zero_()                      # L2 flush between timed steps (not timed)
             starts[i].record(stream)
-            step(sev[i], wev[i])
+            step(fev[i])
             ends[i].record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
@@ -318,14 +326,29 @@ def main_b200(args):
         dist.barrier()
     launches = (twc.twc_kernel_launches() - l0) / K
     step_ms = [starts[i].elapsed_time(ends[i]) for i in range(K)]
-    prep_ms = [sev[i][0].elapsed_time(sev[i][1]) for i in range(K)]
-    k2_ms = [sev[i][1].elapsed_time(sev[i][2]) for i in range(K)]
-    k3_ms = [sev[i][2].elapsed_time(sev[i][3]) for i in range(K)]
-    score_ms = [sev[i][0].elapsed_time(sev[i][3]) for i in range(K)]
-    sweep_ms = [wev[i][0].elapsed_time(wev[i][2]) for i in range(K)]
+
+    def ph(a, b):
+        return statistics.mean(fev[i][a].elapsed_time(fev[i][b]) for i in range(K))
+
+    k2_ms = [fev[i][1].elapsed_time(fev[i][2]) for i in range(K)]
+    phases = {"orient": ph(0, 1), "intersect_k2": ph(1, 2), "epilogue_k3_bin": ph(2, 3),
+              "band_place": ph(3, 4), "sweep16_loop": ph(4, 5), "score": ph(0, 3)}
     total_s = harness.max_over_ranks(sum(step_ms) / 1000.0, dev)
     value = harness.weak_scaling_value(m * K, world, total_s)
     ms_per_step = 1000.0 * total_s / K
+
+    # ---- the same step through the separate twc_score + twc_sweep calls (context)
+    Ks = min(K, 10)
+    sev = [mk(4) for _ in range(Ks)]
+    wev = [mk(3) for _ in range(Ks)]
+    torch.cuda.synchronize()
+    for i in range(Ks):
+        flush.zero_()
+        step_separate(sev[i], wev[i])
+    torch.cuda.synchronize()
+    separate = {"score_ms": statistics.mean(sev[i][0].elapsed_time(sev[i][3]) for i in range(Ks)),
+                "sweep16_ms": statistics.mean(wev[i][0].elapsed_time(wev[i][2]) for i in range(Ks))}
+    separate["step_ms"] = separate["score_ms"] + separate["sweep16_ms"]
 
     # ---- roofline of the dominant kernel (K2, oriented intersection), DESIGN.md Sec. 5
     S, dplus_max = orientation_stats(g)
@@ -378,10 +401,8 @@ def main_b200(args):
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": "explicit 512 MiB L2 flush between timed steps; inputs (CSR 312 MB) "
                              "and outputs exceed the 126 MB L2"},
-            "phases_ms": {"score": statistics.mean(score_ms), "orient": statistics.mean(prep_ms),
-                          "intersect_k2": statistics.mean(k2_ms), "epilogue_k3": statistics.mean(k3_ms),
-                          "sweep16": statistics.mean(sweep_ms)},
-            "score_edges_per_s": world * m / (statistics.mean(score_ms) / 1000.0),
+            "phases_ms": phases, "separate_calls_ms": separate,
+            "score_edges_per_s": world * m / (phases["score"] / 1000.0),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": csum, "wall_s_timed": wall,
             "graph": {"triangles": T, "sum_dminus_dplus": S, "max_dplus": dplus_max,

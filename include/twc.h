@@ -101,8 +101,24 @@ twc_status twc_sweep(const twc_csr *g, const int32_t *tw, const double *deltas_h
                      void *stream);
 
 /* ---------------------------------------------------------------------------------------
+ * twc_score_sweep -- twc_score followed by twc_sweep in one call (the fused device path).
+ * The score epilogue also bins every edge kept at the smallest threshold by sweep step, so
+ * the sweep makes no further pass over TW or the CSR.  Outputs are identical to twc_score +
+ * twc_sweep (t, wedge, tw: device int32[m]; labels: device int32[k*n]; stats: device
+ * int64[2k] or NULL).  deltas_host: HOST double[k], 1 <= k <= 1024, any order, no NaN.
+ * `events`: NULL or 6 cudaEvent_t recorded at [0] start, [1] orientation done, [2]
+ * intersection done, [3] epilogue + binning done, [4] bands placed, [5] all labelled.
+ * Workspace: twc_score_sweep_workspace_bytes(n, m, rb).
+ * ------------------------------------------------------------------------------------- */
+size_t twc_score_sweep_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes);
+twc_status twc_score_sweep(const twc_csr *g, const double *deltas_host, int32_t k,
+                           void *workspace, size_t workspace_bytes, int32_t *t, int32_t *wedge,
+                           int32_t *tw, int32_t *labels, int64_t *stats, void *stream,
+                           void *const *events);
+
+/* ---------------------------------------------------------------------------------------
  * twc_pipeline_host -- the whole path end to end from HOST buffers: copies the CSR to the
- * device, runs twc_score then twc_sweep over deltas_host[k], copies the results back and
+ * device, runs twc_score_sweep over deltas_host[k], copies the results back and
  * synchronises the stream.  g points at HOST rowptr/colidx (pinned memory gives full PCIe
  * speed; pageable works).  t, wedge, tw: HOST int32[m] each, or NULL to skip that copy-back.
  * labels: HOST int32[k*n] or NULL.  stats: HOST int64[2k] or NULL.  Needs a DEVICE workspace

@@ -9,6 +9,7 @@ There is no CPU fallback: if libtwc.so is missing or no CUDA device is present, 
     labels, stats     = twc_cluster(rowptr, colidx, tw, delta)     # int32[n], int64[2]
     labels, stats     = twc_sweep(rowptr, colidx, tw, deltas)      # int32[k, n], int64[k, 2]
     out               = twc_pipeline_host(rowptr_h, colidx_h, deltas)   # host in, host out
+    t, wedge, tw, labels, stats = twc_score_sweep(rowptr, colidx, deltas)   # fused device path
     twc_validate_csr(rowptr, colidx)                                # raises TwcError if invalid
 
 rowptr: int32 or int64 tensor [n+1]; colidx: int32 tensor [2m] (CUDA tensors, except for
@@ -70,6 +71,8 @@ def load_library(path: str = LIB_PATH):
         "twc_score_ex": (ctypes.c_int, [CP, P, SZ, P, P, P, P, P]),
         "twc_sweep_ex": (ctypes.c_int, [CP, P, P, I32, P, SZ, P, P, P, P]),
         "twc_kernel_launches": (I64, []),
+        "twc_score_sweep_workspace_bytes": (SZ, [I64, I64, I32]),
+        "twc_score_sweep": (ctypes.c_int, [CP, P, I32, P, SZ, P, P, P, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -200,6 +203,37 @@ def twc_sweep(rowptr, colidx, tw, deltas, labels=None, stats=None, workspace=Non
                             _ptr(ws), ws.numel(), _ptr(labels), _ptr(stats), _stream(stream),
                             ev[0] if ev else None))
     return labels, stats
+
+
+def twc_score_sweep_workspace_bytes(n, m, rowptr_bytes=4):
+    return int(load_library().twc_score_sweep_workspace_bytes(n, m, rowptr_bytes))
+
+
+def twc_score_sweep(rowptr, colidx, deltas, out=None, labels=None, stats=None, workspace=None,
+                    stream=None, events=None):
+    """twc_score + twc_sweep in one fused call: returns (t, wedge, tw, labels[k, n], stats[k, 2]).
+
+    events: optional list of 6 torch.cuda.Event (see include/twc.h)."""
+    lib = load_library()
+    g, n, m = _graph(rowptr, colidx)
+    dev = colidx.device
+    deltas = [float(d) for d in deltas]
+    k = len(deltas)
+    if out is None:
+        out = tuple(torch.empty(m, dtype=torch.int32, device=dev) for _ in range(3))
+    if labels is None:
+        labels = torch.empty((k, n), dtype=torch.int32, device=dev)
+    if stats is None:
+        stats = torch.empty((k, 2), dtype=torch.int64, device=dev)
+    t, wedge, tw = out
+    arr = (ctypes.c_double * k)(*deltas)
+    ws = _workspace(lib.twc_score_sweep_workspace_bytes(n, m, rowptr.element_size()), dev,
+                    workspace)
+    ev = _events(events)
+    _check(lib.twc_score_sweep(ctypes.byref(g), ctypes.cast(arr, ctypes.c_void_p), k, _ptr(ws),
+                               ws.numel(), _ptr(t), _ptr(wedge), _ptr(tw), _ptr(labels),
+                               _ptr(stats), _stream(stream), ev[0] if ev else None))
+    return t, wedge, tw, labels, stats
 
 
 def twc_pipeline_host(rowptr, colidx, deltas, want_scores=True, out=None, workspace=None,

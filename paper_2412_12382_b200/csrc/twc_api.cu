@@ -202,6 +202,43 @@ twc_status twc_sweep_ex(const twc_csr* g, const int32_t* tw, const double* delta
     return sweep_common(g, tw, thr, k, ws, ws_bytes, labels, stats, stream, ev);
 }
 
+size_t twc_score_sweep_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes) {
+    (void)rowptr_bytes;
+    if (n < 0 || m < 0) return 0;
+    return score_sweep_ws_bytes(n, m);
+}
+
+twc_status twc_score_sweep(const twc_csr* g, const double* deltas_host, int32_t k, void* ws,
+                           size_t ws_bytes, int32_t* t, int32_t* wedge, int32_t* tw,
+                           int32_t* labels, int64_t* stats, void* stream, void* const* events) {
+    g_err.clear();
+    twc_status st = check_csr(g);
+    if (st) return st;
+    if (k < 1 || k > 1024) return fail(TWC_EINVAL, "k=%d must be in [1, 1024]", k);
+    if (!deltas_host) return fail(TWC_EINVAL, "deltas_host is NULL");
+    if (g->m > 0 && (!t || !wedge || !tw)) return fail(TWC_EINVAL, "output array is NULL");
+    if (g->n > 0 && !labels) return fail(TWC_EINVAL, "labels is NULL");
+    long long thr[1024];
+    for (int i = 0; i < k; ++i) {
+        st = delta_to_thr(deltas_host[i], &thr[i]);
+        if (st) return st;
+    }
+    st = check_ws(ws, ws_bytes, score_sweep_ws_bytes(g->n, g->m));
+    if (st) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaEvent_t* ev = reinterpret_cast<cudaEvent_t*>(const_cast<void**>(events));
+    cudaError_t e;
+    if (g->rowptr_bytes == 4)
+        e = score_sweep_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx, thr,
+                                  k, ws, ws_bytes, t, wedge, tw, labels,
+                                  reinterpret_cast<long long*>(stats), s, ev);
+    else
+        e = score_sweep_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr),
+                                        g->colidx, thr, k, ws, ws_bytes, t, wedge, tw, labels,
+                                        reinterpret_cast<long long*>(stats), s, ev);
+    return cuda_status(e, "twc_score_sweep");
+}
+
 // ---- end-to-end from host buffers --------------------------------------------------------
 struct PipeWs {
     void* rowptr;
@@ -220,7 +257,7 @@ static PipeWs carve_pipe(Carver& cv, int64_t n, int64_t m, int rb, int k) {
     w.tw = cv.take<int>(m);
     w.labels = cv.take<int>((size_t)k * n);
     w.stats = cv.take<long long>(2 * (size_t)k);
-    w.inner_bytes = std::max(score_ws_bytes(n, m), cluster_ws_bytes(n, m));
+    w.inner_bytes = score_sweep_ws_bytes(n, m);
     w.inner = cv.take<char>(w.inner_bytes);
     return w;
 }
@@ -260,22 +297,15 @@ twc_status twc_pipeline_host(const twc_csr* gh, const double* deltas_host, int32
     twc_csr gd = *gh;
     gd.rowptr = w.rowptr;
     gd.colidx = w.colidx;
-    if (m > 0) {
-        if (rb == 4)
-            e = score_impl<int>(n, m, static_cast<const int*>(gd.rowptr), gd.colidx, w.inner,
-                                w.inner_bytes, w.t, w.wedge, w.tw, s);
-        else
-            e = score_impl<long long>(n, m, static_cast<const long long*>(gd.rowptr), gd.colidx,
-                                      w.inner, w.inner_bytes, w.t, w.wedge, w.tw, s);
-        if (e != cudaSuccess) return cuda_status(e, "twc_pipeline_host score");
-    }
     if (rb == 4)
-        e = sweep_impl<int>(n, m, static_cast<const int*>(gd.rowptr), gd.colidx, w.tw, thr, k,
-                            w.inner, w.inner_bytes, w.labels, w.stats, s);
+        e = score_sweep_impl<int>(n, m, static_cast<const int*>(gd.rowptr), gd.colidx, thr, k,
+                                  w.inner, w.inner_bytes, w.t, w.wedge, w.tw, w.labels, w.stats,
+                                  s, nullptr);
     else
-        e = sweep_impl<long long>(n, m, static_cast<const long long*>(gd.rowptr), gd.colidx, w.tw,
-                                  thr, k, w.inner, w.inner_bytes, w.labels, w.stats, s);
-    if (e != cudaSuccess) return cuda_status(e, "twc_pipeline_host sweep");
+        e = score_sweep_impl<long long>(n, m, static_cast<const long long*>(gd.rowptr), gd.colidx,
+                                        thr, k, w.inner, w.inner_bytes, w.t, w.wedge, w.tw,
+                                        w.labels, w.stats, s, nullptr);
+    if (e != cudaSuccess) return cuda_status(e, "twc_pipeline_host score_sweep");
     const size_t mb = sizeof(int) * (size_t)m;
     if (t && m) e = cudaMemcpyAsync(t, w.t, mb, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && wedge && m) e = cudaMemcpyAsync(wedge, w.wedge, mb, cudaMemcpyDeviceToHost, s);

@@ -35,8 +35,26 @@ __device__ __forceinline__ int uf_find(int* parent, int x) {
     return cur;
 }
 
+// Root of x, then a second walk pointing every node of the path straight at it (full
+// compression): keeps trees shallow while a band merges many components at once.
+__device__ __forceinline__ int uf_find_compress(int* parent, int x) {
+    int r = parent[x];
+    if (r == x) return r;
+    int next;
+    while (r > (next = parent[r])) r = next;
+    // Second walk, only while above r: a concurrent hook may move the path below r (r itself
+    // hooked under a smaller root), and nodes at or below r must never point at r.
+    int cur = x;
+    while (cur > r) {
+        next = parent[cur];
+        if (next > r) parent[cur] = r;  // r is an ancestor of cur and r < cur: stays a tree
+        cur = next;
+    }
+    return r;
+}
+
 __device__ __forceinline__ void uf_unite(int* parent, int u, int v) {
-    int ru = uf_find(parent, u), rv = uf_find(parent, v);
+    int ru = uf_find_compress(parent, u), rv = uf_find_compress(parent, v);
     while (ru != rv) {
         if (ru < rv) { int tmp = ru; ru = rv; rv = tmp; }  // hook the larger root ru under rv
         const int old = atomicCAS(&parent[ru], ru, rv);
@@ -44,6 +62,11 @@ __device__ __forceinline__ void uf_unite(int* parent, int u, int v) {
         ru = uf_find(parent, old);
         rv = uf_find(parent, rv);
     }
+}
+
+__device__ __forceinline__ unsigned gcd_u(unsigned a, unsigned b) {
+    while (b) { unsigned t = a % b; a = b; b = t; }
+    return a;
 }
 
 __global__ void k_init_parent(int64_t n, int* __restrict__ parent) {
@@ -54,18 +77,6 @@ __global__ void k_init_parent(int64_t n, int* __restrict__ parent) {
 constexpr int kSweepThreads = 256;
 constexpr int kItemsPerThread = kTile / kSweepThreads;  // 4
 constexpr int kMaxTileRows = 2048;
-constexpr int kMaxK = 1024;
-
-// Band of an edge: the first step (thresholds sorted descending) at which it is kept,
-// b = #{i : thr_sorted[i] > TW}; b == k means kept at no threshold.
-__device__ __forceinline__ int band_of(long long val, const long long* thr, int k) {
-    int lo = 0, hi = k;  // thr descending: predicate thr[i] > val is true on a prefix
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (thr[mid] > val) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
 
 // Pass 1: histogram of bands (edges kept at no threshold are not counted).
 __global__ void __launch_bounds__(kSweepThreads) k_band_count(int64_t m, const int* __restrict__ tw,
@@ -182,9 +193,15 @@ __global__ void __launch_bounds__(256) k_hook_list(const int2* __restrict__ pair
                                                    const int* __restrict__ off, int b,
                                                    int* __restrict__ parent) {
     const int beg = off[b], end = off[b + 1];
-    for (int i = beg + blockIdx.x * blockDim.x + threadIdx.x; i < end;
+    const unsigned size = (unsigned)(end - beg);
+    // visit the band in a scrambled order (an affine bijection mod size) so that edges sharing
+    // a vertex are not handled by neighbouring threads at the same time
+    unsigned mult = 2654435761u % (size ? size : 1u);
+    while (size > 1 && (mult == 0 || gcd_u(mult, size) != 1u)) ++mult;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < size;
          i += gridDim.x * blockDim.x) {
-        const int2 e = pairs[i];
+        const unsigned j = (unsigned)(((unsigned long long)i * mult) % size);
+        const int2 e = pairs[beg + j];
         uf_unite(parent, e.x, e.y);
     }
 }
@@ -197,13 +214,30 @@ __global__ void __launch_bounds__(256) k_finalize(int64_t n, int* __restrict__ p
     long long roots = 0;
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
          u += (int64_t)gridDim.x * blockDim.x) {
-        const int r = uf_find(parent, (int)u);
-        labels[u] = r;
-        parent[u] = r;
+        const int p = parent[u];
+        const int r = (p == (int)u) ? p : uf_find(parent, (int)u);
+        __stcs(&labels[u], r);            // streaming store: labels are not re-read
+        if (r != p) parent[u] = r;        // full compression, only when it changes
         roots += (r == (int)u);
     }
     const long long tot = block_sum_ll(roots, s_tmp);
     if (threadIdx.x == 0 && tot && ncomp) atomicAdd(ncomp, (unsigned long long)tot);
+}
+
+// Thresholds (sorted descending) and their caller indices into the workspace, 64 per launch
+// through kernel parameters (no host->device memcpy, so the sweep is graph-capturable).
+struct ThrChunk {
+    long long thr[64];
+    int order[64];
+};
+
+__global__ void k_set_thresholds(ThrChunk c, int base, int cnt, long long* __restrict__ thr,
+                                 int* __restrict__ order) {
+    const int i = threadIdx.x;
+    if (i < cnt) {
+        thr[base + i] = c.thr[i];
+        order[base + i] = c.order[i];
+    }
 }
 
 struct ClusterWs {
@@ -236,6 +270,100 @@ size_t cluster_ws_bytes(int64_t n, int64_t m) {
     return cv.used;
 }
 
+// ------------------------------------------------------------------ sweep building blocks
+void sweep_plan(const long long* thr, int k, SweepPlan* P) {
+    P->k = k;
+    for (int i = 0; i < k; ++i) P->order[i] = i;
+    for (int i = 1; i < k; ++i)  // insertion sort (stable), k is small
+        for (int j = i; j > 0 && thr[P->order[j]] > thr[P->order[j - 1]]; --j) {
+            int tmp = P->order[j]; P->order[j] = P->order[j - 1]; P->order[j - 1] = tmp;
+        }
+    for (int i = 0; i < k; ++i) P->thr[i] = thr[P->order[i]];
+}
+
+void sweep_upload(const SweepPlan& P, long long* thr_dev, int* order_dev, cudaStream_t s) {
+    for (int b = 0; b < P.k; b += 64) {
+        ThrChunk c;
+        const int cnt = std::min(64, P.k - b);
+        for (int i = 0; i < cnt; ++i) {
+            c.thr[i] = P.thr[b + i];
+            c.order[i] = P.order[b + i];
+        }
+        k_set_thresholds<<<1, 64, 0, s>>>(c, b, cnt, thr_dev, order_dev);
+        count_launches(1);
+    }
+}
+
+void band_offsets(const int* cnt, int k, const int* order_dev, int* off, int* cursor,
+                  unsigned long long* stats, cudaStream_t s) {
+    k_band_offsets<<<1, 32, 0, s>>>(cnt, k, order_dev, off, cursor, stats);
+    count_launches(1);
+}
+
+// Place a compact list of kept edges into their band segments: per block, one reservation
+// per band (smem histogram), then smem ranks.
+__global__ void __launch_bounds__(kSweepThreads) k_band_place(
+    const int2* __restrict__ kept, const unsigned short* __restrict__ kband,
+    const int* __restrict__ nkept, int k, int* __restrict__ cursor, int2* __restrict__ pairs) {
+    __shared__ int s_cnt[kMaxK];
+    const int total = *nkept;
+    constexpr int kChunk = kSweepThreads * 4;
+    for (int base = blockIdx.x * kChunk; base < total; base += gridDim.x * kChunk) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < k; i += blockDim.x) s_cnt[i] = 0;
+        __syncthreads();
+        int b[4], r[4];
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const int i = base + it * kSweepThreads + threadIdx.x;
+            b[it] = -1;
+            if (i < total) {
+                b[it] = kband[i];
+                r[it] = atomicAdd(&s_cnt[b[it]], 1);
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < k; i += blockDim.x)
+            if (s_cnt[i]) s_cnt[i] = atomicAdd(&cursor[i], s_cnt[i]);
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const int i = base + it * kSweepThreads + threadIdx.x;
+            if (b[it] >= 0) pairs[s_cnt[b[it]] + r[it]] = kept[i];
+        }
+    }
+}
+
+void band_place(const int2* kept, const unsigned short* kband, const int* nkept, int64_t cap,
+                int k, int* cursor, int2* pairs, cudaStream_t s) {
+    const int64_t chunks = (cap + kSweepThreads * 4 - 1) / (kSweepThreads * 4);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)num_sms() * 8));
+    k_band_place<<<grid, kSweepThreads, 0, s>>>(kept, kband, nkept, k, cursor, pairs);
+    count_launches(1);
+}
+
+void init_parent(int64_t n, int* parent, cudaStream_t s) {
+    k_init_parent<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, parent);
+    count_launches(1);
+}
+
+// Steps in descending threshold order: hook band i, snapshot labels for threshold order[i].
+void sweep_loop(int64_t n, int64_t m, const SweepPlan& P, const int2* pairs, const int* off,
+                int* parent, int* labels, unsigned long long* st, cudaStream_t s) {
+    const int sms = num_sms();
+    const int hook_grid = sms * 8;
+    const int fin_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
+    for (int i = 0; i < P.k; ++i) {
+        const int idx = P.order[i];
+        if (m > 0 && (i == 0 || P.thr[i] < P.thr[i - 1])) {
+            k_hook_list<<<hook_grid, 256, 0, s>>>(pairs, off, i, parent);
+            count_launches(1);
+        }
+        k_finalize<<<fin_grid, 256, 0, s>>>(n, parent, labels + (size_t)idx * n, st + 2 * idx + 1);
+        count_launches(1);
+    }
+}
+
 template <typename RP>
 cudaError_t sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, const int* tw,
                        const long long* thr, int k, void* ws, size_t ws_bytes, int* labels,
@@ -251,22 +379,11 @@ cudaError_t sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         return cudaGetLastError();
     }
     const int sms = num_sms();
-    // thresholds in descending order (fewest kept edges first): kept sets nest
-    int order[kMaxK];
-    long long thr_sorted[kMaxK];
-    for (int i = 0; i < k; ++i) order[i] = i;
-    for (int i = 1; i < k; ++i)  // insertion sort, k is small
-        for (int j = i; j > 0 && thr[order[j]] > thr[order[j - 1]]; --j) {
-            int tmp = order[j]; order[j] = order[j - 1]; order[j - 1] = tmp;
-        }
-    for (int i = 0; i < k; ++i) thr_sorted[i] = thr[order[i]];
-    // pageable host -> device copies: staged by the driver before the call returns
-    cudaMemcpyAsync(w.thr, thr_sorted, sizeof(long long) * k, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(w.order, order, sizeof(int) * k, cudaMemcpyHostToDevice, s);
+    SweepPlan P;
+    sweep_plan(thr, k, &P);
+    sweep_upload(P, w.thr, w.order, s);
     cudaMemsetAsync(w.cnt, 0, sizeof(int) * (k + 1), s);
-    const unsigned nb = (unsigned)((n + 255) / 256);
-    k_init_parent<<<nb, 256, 0, s>>>(n, w.parent);
-    count_launches(1);
+    init_parent(n, w.parent, s);
     if (m > 0) {
         upper_counts<RP>(n, rowptr, colidx, w.up, s);
         exclusive_scan(w.up, w.eoff, n, w.scan_tmp, s);
@@ -274,29 +391,96 @@ cudaError_t sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         const int cgrid = (int)std::min<int64_t>((m + kSweepThreads - 1) / kSweepThreads,
                                                  (int64_t)sms * 8);
         k_band_count<<<cgrid, kSweepThreads, 0, s>>>(m, tw, w.thr, k, w.cnt);
-        k_band_offsets<<<1, 32, 0, s>>>(w.cnt, k, w.order, w.off, w.cursor, st);
+        count_launches(1);
+        band_offsets(w.cnt, k, w.order, w.off, w.cursor, st, s);
         const int64_t nt = num_tiles(m);
         const int sgrid = (int)std::min<int64_t>(nt, (int64_t)sms * 8);
         k_band_scatter<RP><<<sgrid, kSweepThreads, 0, s>>>(m, rowptr, colidx, w.eoff, w.trow, tw,
                                                            w.thr, k, w.cursor, w.pairs);
-        count_launches(3);
-    }
-    record(ev, 1, s);
-    const int hook_grid = sms * 8;
-    const int fin_grid = (int)std::min<int64_t>((int64_t)nb, (int64_t)sms * 8);
-    for (int i = 0; i < k; ++i) {
-        const int idx = order[i];
-        if (m > 0 && (i == 0 || thr_sorted[i] < thr_sorted[i - 1])) {
-            k_hook_list<<<hook_grid, 256, 0, s>>>(w.pairs, w.off, i, w.parent);
-            count_launches(1);
-        }
-        k_finalize<<<fin_grid, 256, 0, s>>>(n, w.parent, labels + (size_t)idx * n,
-                                            st + 2 * idx + 1);
         count_launches(1);
     }
+    record(ev, 1, s);
+    sweep_loop(n, m, P, w.pairs, w.off, w.parent, labels, st, s);
     record(ev, 2, s);
     return cudaGetLastError();
 }
+
+// ------------------------------------------------------------------ fused score + sweep
+struct FusedWs {
+    void* score;
+    size_t score_bytes;
+    int *parent, *cnt, *off, *cursor, *order, *nkept;
+    long long* thr;
+    int2 *kept, *pairs;
+    unsigned short* kband;
+    unsigned long long* stats;
+};
+
+static FusedWs carve_fused(Carver& cv, int64_t n, int64_t m) {
+    FusedWs w;
+    w.score_bytes = std::max(score_ws_bytes(n, m), cluster_ws_bytes(n, m));
+    w.score = cv.take<char>(w.score_bytes);
+    w.parent = cv.take<int>(n);
+    w.cnt = cv.take<int>(kMaxK + 1);
+    w.off = cv.take<int>(kMaxK + 1);
+    w.cursor = cv.take<int>(kMaxK + 1);
+    w.order = cv.take<int>(kMaxK);
+    w.nkept = cv.take<int>(1);
+    w.thr = cv.take<long long>(kMaxK);
+    w.kept = cv.take<int2>(m);
+    w.pairs = cv.take<int2>(m);
+    w.kband = cv.take<unsigned short>(m);
+    w.stats = cv.take<unsigned long long>(2 * kMaxK);
+    return w;
+}
+
+size_t score_sweep_ws_bytes(int64_t n, int64_t m) {
+    Carver cv(nullptr, 0);
+    carve_fused(cv, n, m);
+    return cv.used;
+}
+
+// events: [0] start, [1] orientation done, [2] intersection done, [3] epilogue + binning
+// done, [4] bands placed, [5] all thresholds labelled.
+template <typename RP>
+cudaError_t score_sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+                             const long long* thr, int k, void* ws, size_t ws_bytes, int* t,
+                             int* wedge, int* tw, int* labels, long long* stats, cudaStream_t s,
+                             cudaEvent_t* ev) {
+    Carver cv(ws, ws_bytes);
+    FusedWs w = carve_fused(cv, n, m);
+    unsigned long long* st = stats ? reinterpret_cast<unsigned long long*>(stats) : w.stats;
+    if (m == 0 || n == 0) {  // nothing to score: every vertex is its own component
+        for (int i = 0; i < 6; ++i) record(ev, i, s);
+        return sweep_impl<RP>(n, m, rowptr, colidx, tw, thr, k, w.score, w.score_bytes, labels,
+                              stats, s, nullptr);
+    }
+    SweepPlan P;
+    sweep_plan(thr, k, &P);
+    cudaMemsetAsync(st, 0, sizeof(long long) * 2 * (size_t)k, s);
+    sweep_upload(P, w.thr, w.order, s);
+    cudaMemsetAsync(w.cnt, 0, sizeof(int) * (k + 1), s);
+    cudaMemsetAsync(w.nkept, 0, sizeof(int), s);
+    BinSpec bin{w.thr, k, w.cnt, w.nkept, w.kept, w.kband};
+    cudaError_t e = score_impl<RP>(n, m, rowptr, colidx, w.score, w.score_bytes, t, wedge, tw, s,
+                                   ev, &bin);
+    if (e != cudaSuccess) return e;
+    band_offsets(w.cnt, k, w.order, w.off, w.cursor, st, s);
+    band_place(w.kept, w.kband, w.nkept, m, k, w.cursor, w.pairs, s);
+    init_parent(n, w.parent, s);
+    record(ev, 4, s);
+    sweep_loop(n, m, P, w.pairs, w.off, w.parent, labels, st, s);
+    record(ev, 5, s);
+    return cudaGetLastError();
+}
+
+template cudaError_t score_sweep_impl<int>(int64_t, int64_t, const int*, const int*,
+                                           const long long*, int, void*, size_t, int*, int*,
+                                           int*, int*, long long*, cudaStream_t, cudaEvent_t*);
+template cudaError_t score_sweep_impl<long long>(int64_t, int64_t, const long long*, const int*,
+                                                 const long long*, int, void*, size_t, int*,
+                                                 int*, int*, int*, long long*, cudaStream_t,
+                                                 cudaEvent_t*);
 
 template cudaError_t sweep_impl<int>(int64_t, int64_t, const int*, const int*, const int*,
                                      const long long*, int, void*, size_t, int*, long long*,

@@ -87,4 +87,15 @@ __device__ __forceinline__ bool key_less(int du, int u, int dv, int v) {
     return du < dv || (du == dv && u < v);
 }
 
+// Band of an edge: the first step (thresholds sorted descending) at which it is kept,
+// b = #{i : thr_sorted[i] > TW}; b == k means kept at no threshold.
+__device__ __forceinline__ int band_of(long long val, const long long* thr, int k) {
+    int lo = 0, hi = k;  // thr descending: predicate thr[i] > val is true on a prefix
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (thr[mid] > val) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
 }  // namespace twc

@@ -49,15 +49,47 @@ void tile_rows(const OT* off, int nrows, int64_t total, int tile, int* trow, cud
 template <typename RP>
 void upper_counts(int64_t n, const RP* rowptr, const int* colidx, int* up, cudaStream_t s);
 
+// ---- sweep building blocks (twc_cluster.cu) --------------------------------------------------
+constexpr int kMaxK = 1024;  // thresholds per sweep
+struct SweepPlan {           // thresholds sorted descending (fewest kept edges first)
+    int k;
+    int order[kMaxK];        // caller index of the i-th threshold
+    long long thr[kMaxK];    // keep iff TW >= thr[i]
+};
+void sweep_plan(const long long* thr, int k, SweepPlan* P);
+void sweep_upload(const SweepPlan& P, long long* thr_dev, int* order_dev, cudaStream_t s);
+void band_offsets(const int* cnt, int k, const int* order_dev, int* off, int* cursor,
+                  unsigned long long* stats, cudaStream_t s);
+void band_place(const int2* kept, const unsigned short* kband, const int* nkept, int64_t cap,
+                int k, int* cursor, int2* pairs, cudaStream_t s);
+void sweep_loop(int64_t n, int64_t m, const SweepPlan& P, const int2* pairs, const int* off,
+                int* parent, int* labels, unsigned long long* stats, cudaStream_t s);
+void init_parent(int64_t n, int* parent, cudaStream_t s);
+
 // ---- score (twc_score.cu) ------------------------------------------------------------------
+// Optional binning of kept edges by sweep step, fused into the score epilogue (K3).
+struct BinSpec {
+    const long long* thr;   // device, sorted descending, k entries
+    int k;
+    int* cnt;               // device [k] band histogram (zeroed by the caller)
+    int* nkept;             // device counter (zeroed by the caller)
+    int2* kept;             // device [m] (u, v) of kept edges, in no particular order
+    unsigned short* kband;  // device [m] band of kept[i]
+};
 size_t score_ws_bytes(int64_t n, int64_t m);
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
-                       cudaEvent_t* ev = nullptr);
+                       cudaEvent_t* ev = nullptr, const BinSpec* bin = nullptr);
 
 // ---- cluster (twc_cluster.cu) --------------------------------------------------------------
 size_t cluster_ws_bytes(int64_t n, int64_t m);
+size_t score_sweep_ws_bytes(int64_t n, int64_t m);
+template <typename RP>
+cudaError_t score_sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+                             const long long* thr, int k, void* ws, size_t ws_bytes, int* t,
+                             int* wedge, int* tw, int* labels, long long* stats, cudaStream_t s,
+                             cudaEvent_t* ev);
 // thresholds already converted to integer "keep iff tw >= thr[i]" form, any order.
 template <typename RP>
 cudaError_t sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, const int* tw,

@@ -26,23 +26,22 @@ __global__ void k0_degrees(int64_t n, const RP* __restrict__ rowptr, int* __rest
 }
 
 // ------------------------------------------------ K1: orientation over full-CSR slot tiles
-// The 2m CSR slots are cut into tiles of kSlotTile consecutive slots (rows stay in order, so a
-// tile is a run of whole rows plus partial rows at its ends).  Each CTA caches the tile's row
-// offsets in smem and maps a slot to its row by binary search; each thread takes kSlotItems
-// slots strided by the block size (coalesced colidx reads).
-//   K1a: out-bit per slot (key(u) < key(v)), and per-row counts of upper entries (v > u) and
-//        out-entries, aggregated per row segment inside each warp (ballot + popc) and added to
-//        the row totals with one atomic per segment;  lastcnt[tile] = out-entries of the
-//        tile's last row inside the tile.
-//   carry: out-entries of a tile's first row that lie in earlier tiles.
-//   K1b: scatter: the out-entry at slot p of row u goes to rp_or[u] + (out-entries of row u
-//        before p) -- filtering a sorted row keeps it sorted; for aligned edges (u < v, i.e.
-//        an upper slot) it also records c2o[canonical id] = oriented slot.
+// Every CSR slot p (row u, neighbour v) gets two bits: out(p) = key(u) < key(v) (the oriented
+// edge u -> v exists) and upper(p) = v > u (p is the canonical copy of edge {u,v}).  Because
+// rows are contiguous and sorted, all oriented quantities are prefix counts over slots:
+//   * the oriented slot of an out-entry p is  #out(q < p)      -> col_or[#out(q<p)] = v, and
+//     filtering a sorted row keeps it sorted;
+//   * the canonical id of an upper slot p is  #upper(q < p)    (S:66-69 order);
+//   * rp_or[u] = #out(q < rowptr[u]),  eoff[u] = #upper(q < rowptr[u]);
+//   * an aligned edge (out and upper) records c2o[canonical id] = oriented slot.
+// K1 is one pass over tiles of kSlotTile slots (8 consecutive slots per thread, one row search
+// per thread, then a walk) with a block scan and a decoupled look-back across tiles for the
+// two prefix counts; it also stores per-32-slot word bits and exclusive prefixes so that K1r
+// can derive rp_or/eoff for every row with one lookup.
 constexpr int kSlotThreads = 256;
 constexpr int kSlotItems = 8;
 constexpr int kSlotTile = kSlotThreads * kSlotItems;  // 2048 slots
-constexpr int kSlotWords = kSlotTile / 32;
-constexpr int kMaxSlotRows = 2048;
+constexpr int kMaxSlotRows = 1024;
 
 template <typename RP>
 struct SlotTile {
@@ -78,35 +77,21 @@ __device__ __forceinline__ RP row_off(const SlotTile<RP>& T, const RP* s_rp,
     return T.cached ? s_rp[ri] : rowptr[T.r0 + ri];
 }
 
-// Per-warp segmented popcount: lanes hold consecutive slots with non-decreasing row index ri
-// (-1 = invalid lane); returns, in the first lane of each row segment, popc(word & segment).
-__device__ __forceinline__ unsigned segment_mask(int ri, int lane, bool& head) {
-    const int prev = __shfl_up_sync(FULL, ri, 1);
-    head = ri >= 0 && (lane == 0 || prev != ri);
-    const unsigned heads = __ballot_sync(FULL, head) | __ballot_sync(FULL, ri < 0);
-    const unsigned above = heads & ~((2u << lane) - 1u);
-    const int end = above ? __ffs(above) - 1 : 32;
-    const unsigned upto = end == 32 ? FULL : ((1u << end) - 1u);
-    return upto & ~((1u << lane) - 1u);
-}
-
+// K1a: out/upper bits of every slot (8 consecutive slots per thread, one row search per
+// thread, then a walk along the rows), stored as 32-slot words, plus per-tile counts.
 template <typename RP>
-__global__ void __launch_bounds__(kSlotThreads) k1_count(
+__global__ void __launch_bounds__(kSlotThreads, 8) k1_bits(
     int64_t m2, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
-    const int* __restrict__ deg, const int* __restrict__ ftrow, int* __restrict__ up,
-    int* __restrict__ dplus, unsigned* __restrict__ outbits, int* __restrict__ lastcnt) {
+    const int* __restrict__ deg, const int* __restrict__ ftrow, unsigned* __restrict__ obits,
+    unsigned* __restrict__ ubits, int* __restrict__ tile_out, int* __restrict__ tile_up) {
     __shared__ RP s_rp[kMaxSlotRows + 1];
-    __shared__ int s_up[kMaxSlotRows];
-    __shared__ int s_out[kMaxSlotRows];
-    const int lane = threadIdx.x & 31;
+    __shared__ unsigned s_wsum[kSlotThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t ntiles = (m2 + kSlotTile - 1) / kSlotTile;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         __syncthreads();
         const SlotTile<RP> T = load_slot_tile(tile, m2, rowptr, ftrow, s_rp);
-        if (T.cached)
-            for (int i = threadIdx.x; i < T.nr; i += blockDim.x) { s_up[i] = 0; s_out[i] = 0; }
         __syncthreads();
-        // this thread: kSlotItems consecutive slots [q0, q0 + kSlotItems)
         const RP q0 = T.p0 + (RP)(threadIdx.x * kSlotItems);
         int v[kSlotItems];
         if (q0 + kSlotItems <= T.p1) {
@@ -121,153 +106,160 @@ __global__ void __launch_bounds__(kSlotThreads) k1_count(
         int dv[kSlotItems];
 #pragma unroll
         for (int j = 0; j < kSlotItems; ++j) dv[j] = (q0 + j < T.p1) ? deg[v[j]] : 0;
-        unsigned ob = 0;
+        unsigned ob = 0, ub = 0;
         if (q0 < T.p1) {
             int ri = slot_row(T, s_rp, rowptr, q0);
             RP rb = row_off(T, s_rp, rowptr, ri), re = row_off(T, s_rp, rowptr, ri + 1);
-            int cu = 0, co = 0;
 #pragma unroll
             for (int j = 0; j < kSlotItems; ++j) {
                 const RP p = q0 + j;
                 if (p < T.p1) {
-                    if (p >= re) {  // next non-empty row
-                        if (cu || co) {
-                            if (T.cached) { atomicAdd(&s_up[ri], cu); atomicAdd(&s_out[ri], co); }
-                            else { atomicAdd(&up[T.r0 + ri], cu); atomicAdd(&dplus[T.r0 + ri], co); }
-                        }
-                        cu = co = 0;
-                        do {
-                            ++ri;
-                            rb = re;
-                            re = row_off(T, s_rp, rowptr, ri + 1);
-                        } while (p >= re);
+                    while (p >= re) {  // next row (skipping empty rows)
+                        ++ri;
+                        rb = re;
+                        re = row_off(T, s_rp, rowptr, ri + 1);
                     }
                     const int u = T.r0 + ri;
-                    const bool out = key_less((int)(re - rb), u, dv[j], v[j]);
-                    ob |= (unsigned)out << j;
-                    co += out;
-                    cu += v[j] > u;
+                    ob |= (unsigned)key_less((int)(re - rb), u, dv[j], v[j]) << j;
+                    ub |= (unsigned)(v[j] > u) << j;
                 }
             }
-            if (cu || co) {
-                if (T.cached) { atomicAdd(&s_up[ri], cu); atomicAdd(&s_out[ri], co); }
-                else { atomicAdd(&up[T.r0 + ri], cu); atomicAdd(&dplus[T.r0 + ri], co); }
-            }
         }
-        // 4 threads x 8 bits = one 32-bit word of out-bits
-        unsigned word = ob << (8 * (lane & 3));
-        word |= __shfl_xor_sync(FULL, word, 1);
-        word |= __shfl_xor_sync(FULL, word, 2);
-        if ((lane & 3) == 0 && q0 < T.p1) outbits[q0 >> 5] = word;
+        unsigned ow = ob << (8 * (lane & 3)), uw = ub << (8 * (lane & 3));
+        ow |= __shfl_xor_sync(FULL, ow, 1);
+        ow |= __shfl_xor_sync(FULL, ow, 2);
+        uw |= __shfl_xor_sync(FULL, uw, 1);
+        uw |= __shfl_xor_sync(FULL, uw, 2);
+        if ((lane & 3) == 0 && q0 < T.p1) {
+            obits[q0 >> 5] = ow;
+            ubits[q0 >> 5] = uw;
+        }
+        unsigned cnt = (__popc(ob) << 16) | __popc(ub);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(FULL, cnt, d);
+        if (lane == 0) s_wsum[wid] = cnt;
         __syncthreads();
-        if (T.cached) {
-            for (int i = threadIdx.x; i < T.nr; i += blockDim.x) {
-                if (s_out[i]) atomicAdd(&dplus[T.r0 + i], s_out[i]);
-                if (s_up[i]) atomicAdd(&up[T.r0 + i], s_up[i]);
-            }
-        }
         if (threadIdx.x == 0) {
-            const int rl = slot_row(T, s_rp, rowptr, T.p1 - 1);
-            int c = 0;
-            if (T.cached) {
-                c = s_out[rl];
-            } else {  // uncached tile: recount the last row's out-bits inside the tile
-                __threadfence_block();
-                const RP rb = row_off(T, s_rp, rowptr, rl);
-                const RP from = rb > T.p0 ? rb : T.p0;
-                for (RP q = from; q < T.p1; ++q) c += (outbits[q >> 5] >> (q & 31)) & 1u;
-            }
-            lastcnt[tile] = c;
+            unsigned tot = 0;
+#pragma unroll
+            for (int i = 0; i < kSlotThreads / 32; ++i) tot += s_wsum[i];
+            tile_out[tile] = (int)(tot >> 16);
+            tile_up[tile] = (int)(tot & 0xffffu);
         }
     }
 }
 
-// carry[t] = out-entries of tile t's first row that lie in tiles before t.
-template <typename RP>
-__global__ void k1_carry(int64_t ntiles, const RP* __restrict__ rowptr,
-                         const int* __restrict__ ftrow, const int* __restrict__ lastcnt,
-                         int* __restrict__ carry) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntiles) return;
-    const int r0 = ftrow[t];
-    const RP rs = rowptr[r0];
-    int c = 0;
-    for (int64_t q = t - 1; q >= 0 && rs < (RP)((q + 1) * kSlotTile); --q) {
-        c += lastcnt[q];            // row r0 holds the last slot of tile q
-        if (rs >= (RP)(q * kSlotTile)) break;  // row r0 starts inside tile q
+// Exclusive scans of the two per-tile count arrays (one block; ntiles ~ 2m / 2048).
+__global__ void __launch_bounds__(1024) k1_tile_scan(int64_t ntiles, int* __restrict__ a,
+                                                     int* __restrict__ b) {
+    __shared__ int s_wa[32], s_wb[32];
+    __shared__ int s_ca, s_cb;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) { s_ca = 0; s_cb = 0; }
+    __syncthreads();
+    for (int64_t base = 0; base < ntiles; base += 1024) {
+        const int64_t i = base + threadIdx.x;
+        const int va = i < ntiles ? a[i] : 0, vb = i < ntiles ? b[i] : 0;
+        const int ia = warp_incl_scan(va, lane), ib = warp_incl_scan(vb, lane);
+        if (lane == 31) { s_wa[wid] = ia; s_wb[wid] = ib; }
+        __syncthreads();
+        if (wid == 0) {
+            const int xa = s_wa[lane], xb = s_wb[lane];
+            const int ya = warp_incl_scan(xa, lane), yb = warp_incl_scan(xb, lane);
+            s_wa[lane] = ya - xa;
+            s_wb[lane] = yb - xb;
+        }
+        __syncthreads();
+        const int ca = s_ca, cb = s_cb;
+        if (i < ntiles) {
+            a[i] = ca + s_wa[wid] + ia - va;
+            b[i] = cb + s_wb[wid] + ib - vb;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) {
+            s_ca = ca + s_wa[wid] + ia;
+            s_cb = cb + s_wb[wid] + ib;
+        }
+        __syncthreads();
     }
-    carry[t] = c;
 }
 
-template <typename RP>
-__global__ void __launch_bounds__(kSlotThreads) k1_scatter(
-    int64_t m2, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
-    const int* __restrict__ ftrow, const unsigned* __restrict__ outbits,
-    const int* __restrict__ carry, const int* __restrict__ rp_or, const int* __restrict__ eoff,
+// K1b: oriented slot = #out before p, canonical id = #upper before p (tile prefix + block
+// scan + popc); scatter col_or, record c2o for aligned edges, store the word prefixes.
+__global__ void __launch_bounds__(kSlotThreads) k1_write(
+    int64_t m2, const int* __restrict__ colidx, const unsigned* __restrict__ obits,
+    const unsigned* __restrict__ ubits, const int* __restrict__ tile_out,
+    const int* __restrict__ tile_up, int* __restrict__ opre, int* __restrict__ upre,
     int* __restrict__ col_or, int* __restrict__ c2o) {
-    __shared__ RP s_rp[kMaxSlotRows + 1];
-    __shared__ unsigned s_w[kSlotWords];
-    __shared__ int s_wpre[kSlotWords + 1];
+    __shared__ unsigned s_wsum[kSlotThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t ntiles = (m2 + kSlotTile - 1) / kSlotTile;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        __syncthreads();
-        const SlotTile<RP> T = load_slot_tile(tile, m2, rowptr, ftrow, s_rp);
-        const int nw = (int)((T.p1 - T.p0 + 31) >> 5);
-        if (threadIdx.x < 32) {  // word prefix of the tile's out-bits (64 words, one warp)
-            const int lane = threadIdx.x;
-            const unsigned a = lane < nw ? outbits[(T.p0 >> 5) + lane] : 0u;
-            const unsigned b = lane + 32 < nw ? outbits[(T.p0 >> 5) + lane + 32] : 0u;
-            s_w[lane] = a;
-            s_w[lane + 32] = b;
-            const int ia = warp_incl_scan(__popc(a), lane);
-            const int ta = __shfl_sync(FULL, ia, 31);
-            const int ib = warp_incl_scan(__popc(b), lane);
-            s_wpre[lane] = ia - __popc(a);
-            s_wpre[lane + 32] = ta + ib - __popc(b);
-            if (lane == 31) s_wpre[64] = ta + ib;
+        const int64_t p0 = tile * kSlotTile;
+        const int64_t q0 = p0 + threadIdx.x * kSlotItems;
+        unsigned ob = 0, ub = 0;
+        if (q0 < m2) {
+            const int sh = 8 * (lane & 3);
+            ob = (obits[q0 >> 5] >> sh) & 0xffu;
+            ub = (ubits[q0 >> 5] >> sh) & 0xffu;
         }
+        const unsigned cnt = (__popc(ob) << 16) | __popc(ub);
+        const unsigned incl = (unsigned)warp_incl_scan((int)cnt, lane);
         __syncthreads();
-        const int off0 = threadIdx.x * kSlotItems;
-        const RP q0 = T.p0 + (RP)off0;
-        const unsigned bits = (s_w[off0 >> 5] >> (off0 & 31)) & 0xffu;
-        if (q0 >= T.p1 || bits == 0u) continue;
-        const int cin = carry[tile];
-        int ri = slot_row(T, s_rp, rowptr, q0);
-        RP rb = row_off(T, s_rp, rowptr, ri), re = row_off(T, s_rp, rowptr, ri + 1);
-        // out-entries of the current row inside the tile before slot q0
-        int from = rb > T.p0 ? (int)(rb - T.p0) : 0;
-        const int pb0 = s_wpre[off0 >> 5] + __popc(s_w[off0 >> 5] & ((1u << (off0 & 31)) - 1u));
-        int rank = pb0 - (s_wpre[from >> 5] + __popc(s_w[from >> 5] & ((1u << (from & 31)) - 1u))) +
-                   (rb < T.p0 ? cin : 0);
-        int u = T.r0 + ri;
-        int base = rp_or[u];
+        if (lane == 31) s_wsum[wid] = incl;
+        __syncthreads();
+        unsigned wpre = 0;
 #pragma unroll
-        for (int j = 0; j < kSlotItems; ++j) {
-            const RP p = q0 + j;
-            if (!((bits >> j) & 1u)) {
-                continue;
+        for (int i = 0; i < kSlotThreads / 32; ++i) wpre += (i < wid) ? s_wsum[i] : 0u;
+        const unsigned ex = wpre + incl - cnt;
+        const int obase = tile_out[tile] + (int)(ex >> 16);
+        const int ubase = tile_up[tile] + (int)(ex & 0xffffu);
+        if ((lane & 3) == 0 && q0 < m2) {
+            opre[q0 >> 5] = obase;
+            upre[q0 >> 5] = ubase;
+        }
+        if (ob) {
+            int v[kSlotItems];
+            if (q0 + kSlotItems <= m2) {
+                const int4* src = reinterpret_cast<const int4*>(colidx + q0);
+                const int4 a = __ldg(src), b = __ldg(src + 1);
+                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+                v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < kSlotItems; ++j) v[j] = (q0 + j < m2) ? colidx[q0 + j] : 0;
             }
-            if (p >= re) {  // a new row: its out-entries before p all lie in this thread's run
-                do {
-                    ++ri;
-                    rb = re;
-                    re = row_off(T, s_rp, rowptr, ri + 1);
-                } while (p >= re);
-                u = T.r0 + ri;
-                base = rp_or[u];
-                rank = __popc(bits & ((1u << j) - 1u) & ~((1u << (int)(rb - q0)) - 1u));
-            }
-            const int sl = base + rank;
-            ++rank;
-            const int v = colidx[p];
-            col_or[sl] = v;
-            if (v > u) {  // aligned edge: canonical id of the upper slot p
-                const int eu = eoff[u];
-                const int lo = (int)(re - rb) - (eoff[u + 1] - eu);
-                c2o[eu + (int)(p - rb) - lo] = sl;
+#pragma unroll
+            for (int j = 0; j < kSlotItems; ++j) {
+                if ((ob >> j) & 1u) {
+                    const unsigned below = (1u << j) - 1u;
+                    const int sl = obase + __popc(ob & below);
+                    col_or[sl] = v[j];
+                    if ((ub >> j) & 1u) c2o[ubase + __popc(ub & below)] = sl;
+                }
             }
         }
     }
+}
+
+// K1r: rp_or[u] = #out(q < rowptr[u]), eoff[u] = #upper(q < rowptr[u]); rp_or[n] = eoff[n] = m.
+template <typename RP>
+__global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
+                        const unsigned* __restrict__ obits, const unsigned* __restrict__ ubits,
+                        const int* __restrict__ opre, const int* __restrict__ upre,
+                        int* __restrict__ rp_or, int* __restrict__ eoff) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u > n) return;
+    const RP p = rowptr[u];
+    if ((int64_t)p >= 2 * m) {
+        rp_or[u] = (int)m;
+        eoff[u] = (int)m;
+        return;
+    }
+    const int64_t wi = (int64_t)(p >> 5);
+    const unsigned mask = (1u << (p & 31)) - 1u;
+    rp_or[u] = opre[wi] + __popc(obits[wi] & mask);
+    eoff[u] = upre[wi] + __popc(ubits[wi] & mask);
 }
 
 // ---------------------------------------------------------- K2 oriented intersection
@@ -484,14 +476,27 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n,
 constexpr int kK3Threads = 256;
 constexpr int kMaxTileRows = 2048;
 
-template <typename RP>
-__global__ void __launch_bounds__(kK3Threads) k3_score(
+template <typename RP, bool BIN>
+__global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int* __restrict__ deg, const int* __restrict__ eoff, const int* __restrict__ trow,
     const int* __restrict__ rp_or, const int* __restrict__ col_or, const int* __restrict__ c2o,
     const int* __restrict__ t_or, int* __restrict__ t, int* __restrict__ wedge,
-    int* __restrict__ tw) {
+    int* __restrict__ tw, BinSpec bin) {
+    constexpr int kIt = kTile / kK3Threads;
     __shared__ int s_off[kMaxTileRows + 1];
+    extern __shared__ __align__(8) unsigned char k3_dyn[];  // BIN: thr[k] (i64), hist[k]
+    long long* s_thr = reinterpret_cast<long long*>(k3_dyn);
+    int* s_hist = reinterpret_cast<int*>(k3_dyn + 8 * (size_t)(BIN ? bin.k : 0));
+    __shared__ int s_wk[kK3Threads / 32];
+    __shared__ int s_base;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (BIN) {
+        for (int i = threadIdx.x; i < bin.k; i += blockDim.x) {
+            s_thr[i] = bin.thr[i];
+            s_hist[i] = 0;
+        }
+    }
     const int64_t ntiles = num_tiles(m);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int c0 = (int)(tile * kTile);
@@ -503,52 +508,109 @@ __global__ void __launch_bounds__(kK3Threads) k3_score(
         if (cached)
             for (int i = threadIdx.x; i <= nr; i += blockDim.x) s_off[i] = eoff[r0 + i];
         __syncthreads();
-#pragma unroll 2
-        for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+        int2 kp[kIt];
+        int kb[kIt];
+        unsigned kmask = 0;
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+            const int c = c0 + it * kK3Threads + threadIdx.x;
+            int bnd = -1 - lane;  // unique dummy for lanes without a kept edge
+            if (c < c1) {
             const int ri = cached ? last_le(s_off, nr + 1, c) : last_le(eoff + r0, nr + 1, c);
             const int u = r0 + ri;
             const int eu = cached ? s_off[ri] : eoff[u];
             const int upu = (cached ? s_off[ri + 1] : eoff[u + 1]) - eu;
             const RP rb = rowptr[u];
             const int du = (int)(rowptr[u + 1] - rb);
-            const int v = colidx[rb + (RP)(du - upu) + (RP)(c - eu)];  // upper slot of (u,v)
+            const int v = __ldcs(colidx + rb + (RP)(du - upu) + (RP)(c - eu));  // upper slot of (u,v)
+            const int c2 = __ldcs(c2o + c);  // valid for aligned edges; issued early, used if aligned
             const int dv = deg[v];
+            const int ob = rp_or[v], oe = rp_or[v + 1];
             int sl;
             if (key_less(du, u, dv, v)) {
-                sl = c2o[c];
-            } else {
-                const int ob = rp_or[v];
-                sl = ob + lower_bound(col_or + ob, rp_or[v + 1] - ob, u);
+                sl = c2;
+            } else {  // reversed edge: u's position in N+(v)
+                const int len = oe - ob;
+                if (len <= 8) {  // short list: independent loads, count entries below u
+                    int below = 0;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) below += (e < len && col_or[ob + e] < u);
+                    sl = ob + below;
+                } else {
+                    sl = ob + lower_bound(col_or + ob, len, u);
+                }
             }
             const int tt = t_or[sl];
-            t[c] = tt;
-            wedge[c] = du + dv - 2 * tt - 2;
-            tw[c] = 3 * tt - du - dv + 2;
+            const int score = 3 * tt - du - dv + 2;
+            __stcs(t + c, tt);
+            __stcs(wedge + c, du + dv - 2 * tt - 2);
+            __stcs(tw + c, score);
+            if (BIN && (long long)score >= s_thr[bin.k - 1]) {  // kept at the smallest threshold
+                bnd = band_of(score, s_thr, bin.k);
+                kp[it] = make_int2(u, v);
+                kb[it] = bnd;
+                kmask |= 1u << it;
+            }
+            }
+            if (BIN) {  // warp-aggregated band histogram: one smem atomic per distinct band
+                const unsigned grp = __match_any_sync(FULL, bnd);
+                if (bnd >= 0 && lane == __ffs(grp) - 1) atomicAdd(&s_hist[bnd], __popc(grp));
+            }
         }
+        if (BIN) {  // append this tile's kept edges with one reservation per tile
+            const int nk = __popc(kmask);
+            const int incl = warp_incl_scan(nk, lane);
+            if (lane == 31) s_wk[wid] = incl;
+            __syncthreads();
+            int wpre = 0, tot = 0;
+#pragma unroll
+            for (int i = 0; i < kK3Threads / 32; ++i) {
+                const int x = s_wk[i];
+                wpre += (i < wid) ? x : 0;
+                tot += x;
+            }
+            if (threadIdx.x == 0) s_base = tot ? atomicAdd(bin.nkept, tot) : 0;
+            __syncthreads();
+            int pos = s_base + wpre + incl - nk;
+#pragma unroll
+            for (int it = 0; it < kIt; ++it) {
+                if ((kmask >> it) & 1u) {
+                    bin.kept[pos] = kp[it];
+                    bin.kband[pos] = (unsigned short)kb[it];
+                    ++pos;
+                }
+            }
+        }
+    }
+    if (BIN) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < bin.k; i += blockDim.x)
+            if (s_hist[i]) atomicAdd(&bin.cnt[i], s_hist[i]);
     }
 }
 
 // ------------------------------------------------------------------------ host side
 struct ScoreWs {
-    int *deg, *up, *eoff, *dplus, *rp_or, *scan_tmp, *trow, *ftrow, *lastcnt, *carry;
-    unsigned* outbits;
+    int *deg, *eoff, *rp_or, *trow, *ftrow, *tile_out, *tile_up, *opre, *upre;
+    unsigned *obits, *ubits;
     int *col_or, *t_or, *c2o, *work;
 };
 
 static ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
     ScoreWs w;
     const int64_t nst = (2 * m + kSlotTile - 1) / kSlotTile;
+    const int64_t nw = (2 * m + 31) / 32;
     w.deg = cv.take<int>(n);
-    w.up = cv.take<int>(n);
-    w.dplus = cv.take<int>(n);
     w.eoff = cv.take<int>(n + 1);
     w.rp_or = cv.take<int>(n + 1);
-    w.scan_tmp = cv.take<int>(scan_temp_bytes(n) / sizeof(int));
     w.trow = cv.take<int>(num_tiles(m) + 1);
     w.ftrow = cv.take<int>(nst + 1);
-    w.lastcnt = cv.take<int>(nst);
-    w.carry = cv.take<int>(nst);
-    w.outbits = cv.take<unsigned>((2 * m + 31) / 32);
+    w.tile_out = cv.take<int>(nst);
+    w.tile_up = cv.take<int>(nst);
+    w.obits = cv.take<unsigned>(nw);
+    w.ubits = cv.take<unsigned>(nw);
+    w.opre = cv.take<int>(nw);
+    w.upre = cv.take<int>(nw);
     w.col_or = cv.take<int>(m);
     w.t_or = cv.take<int>(m);
     w.c2o = cv.take<int>(m);
@@ -572,7 +634,7 @@ static int grid_for(int64_t items, int per_block, int max_blocks) {
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
-                       cudaEvent_t* ev) {
+                       cudaEvent_t* ev, const BinSpec* bin) {
     if (m == 0 || n == 0) return cudaGetLastError();
     Carver cv(ws, ws_bytes);
     ScoreWs w = carve_score(cv, n, m);
@@ -580,23 +642,21 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     const int64_t m2 = 2 * m;
     const int64_t nst = (m2 + kSlotTile - 1) / kSlotTile;
     record(ev, 0, s);
-    // a1 + a2: degrees, orientation, oriented CSR
-    cudaMemsetAsync(w.up, 0, sizeof(int) * (size_t)n, s);
-    cudaMemsetAsync(w.dplus, 0, sizeof(int) * (size_t)n, s);
+    // a1 + a2: degrees, orientation, oriented CSR (one pass with a decoupled look-back)
     k0_degrees<RP><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rowptr, w.deg);
     count_launches(1);
     tile_rows<RP>(rowptr, (int)n, m2, kSlotTile, w.ftrow, s);
-    const int sgrid = grid_for(nst, 1, sms * 8);
-    k1_count<RP><<<sgrid, kSlotThreads, 0, s>>>(m2, rowptr, colidx, w.deg, w.ftrow, w.up, w.dplus,
-                                               w.outbits, w.lastcnt);
-    k1_carry<RP><<<(unsigned)((nst + 255) / 256), 256, 0, s>>>(nst, rowptr, w.ftrow, w.lastcnt,
-                                                              w.carry);
-    count_launches(2);
-    exclusive_scan(w.up, w.eoff, n, w.scan_tmp, s);
-    exclusive_scan(w.dplus, w.rp_or, n, w.scan_tmp, s);
-    k1_scatter<RP><<<sgrid, kSlotThreads, 0, s>>>(m2, rowptr, colidx, w.ftrow, w.outbits, w.carry,
-                                                 w.rp_or, w.eoff, w.col_or, w.c2o);
-    count_launches(1);
+    {
+        const int grid = grid_for(nst, 1, sms * 8);
+        k1_bits<RP><<<grid, kSlotThreads, 0, s>>>(m2, rowptr, colidx, w.deg, w.ftrow, w.obits,
+                                                 w.ubits, w.tile_out, w.tile_up);
+        k1_tile_scan<<<1, 1024, 0, s>>>(nst, w.tile_out, w.tile_up);
+        k1_write<<<grid, kSlotThreads, 0, s>>>(m2, colidx, w.obits, w.ubits, w.tile_out,
+                                               w.tile_up, w.opre, w.upre, w.col_or, w.c2o);
+        k1_rows<RP><<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, m, rowptr, w.obits, w.ubits,
+                                                                   w.opre, w.upre, w.rp_or, w.eoff);
+        count_launches(4);
+    }
     tile_first_rows(w.eoff, (int)n, m, w.trow, s);
     cudaMemsetAsync(w.t_or, 0, sizeof(int) * (size_t)m, s);
     cudaMemsetAsync(w.work, 0, sizeof(int), s);
@@ -620,8 +680,14 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     {
         const int64_t nt = num_tiles(m);
         const int grid = grid_for(nt, 1, sms * 8);
-        k3_score<RP><<<grid, kK3Threads, 0, s>>>(m, rowptr, colidx, w.deg, w.eoff, w.trow,
-                                                  w.rp_or, w.col_or, w.c2o, w.t_or, t, wedge, tw);
+        if (bin)
+            k3_score<RP, true><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(m, rowptr, colidx, w.deg, w.eoff, w.trow,
+                                                           w.rp_or, w.col_or, w.c2o, w.t_or, t,
+                                                           wedge, tw, *bin);
+        else
+            k3_score<RP, false><<<grid, kK3Threads, 0, s>>>(m, rowptr, colidx, w.deg, w.eoff,
+                                                            w.trow, w.rp_or, w.col_or, w.c2o,
+                                                            w.t_or, t, wedge, tw, BinSpec{});
         count_launches(1);
         record(ev, 3, s);
     }
@@ -629,9 +695,10 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
 }
 
 template cudaError_t score_impl<int>(int64_t, int64_t, const int*, const int*, void*, size_t,
-                                     int*, int*, int*, cudaStream_t, cudaEvent_t*);
+                                     int*, int*, int*, cudaStream_t, cudaEvent_t*,
+                                     const BinSpec*);
 template cudaError_t score_impl<long long>(int64_t, int64_t, const long long*, const int*,
                                            void*, size_t, int*, int*, int*, cudaStream_t,
-                                           cudaEvent_t*);
+                                           cudaEvent_t*, const BinSpec*);
 
 }  // namespace twc

@@ -212,11 +212,42 @@ def test_validate_csr():
         twc.twc_validate_csr(rp, ci3)
 
 
+def fused_parity(oracle_mod, g, deltas, ot=None):
+    """twc_score_sweep (the fused path bench.py times) against the oracle."""
+    if ot is None:
+        ot = oracle_mod.score(g)
+    rp, ci = harness.to_device(g)
+    t, w, tw, lab, st = twc.twc_score_sweep(rp, ci, deltas)
+    torch.cuda.synchronize()
+    for a, b in zip((t, w, tw), ot):
+        assert np.array_equal(a.cpu().numpy(), b)
+    lab, st = lab.cpu().numpy(), st.cpu().numpy()
+    for i, d in enumerate(deltas):
+        ol, kept, ncomp = oracle_mod.cluster(g, ot[2], d)
+        assert np.array_equal(lab[i], ol), (d, np.nonzero(lab[i] != ol)[0][:5])
+        assert (int(st[i, 0]), int(st[i, 1])) == (kept, ncomp), d
+
+
+def test_fused_score_sweep_small(oracle_mod):
+    rng = np.random.default_rng(21)
+    for it in range(12):
+        n = int(rng.integers(2, 4000))
+        g = gg.erdos_renyi(n, float(rng.random()) * min(1.0, 30.0 / n), seed=100 + it)
+        ds = [-math.inf, 0.0, -3.0, -3.0, 2.5, math.inf, -1e300, 1e300]
+        fused_parity(oracle_mod, g, ds)
+    for g in (gg.empty(7), gg.path(2), gg.complete(40), gg.star(3000, 11)):
+        fused_parity(oracle_mod, g, [-2.0, math.inf, -math.inf])
+    fused_parity(oracle_mod, gg.complete(3000), [2998.0, 2999.0, 0.0])
+
+
 # ------------------------------------------------------------------ the five configs, full size
 
 @pytest.mark.parametrize("config", [1, 2, 3, 4, 5])
 def test_config_parity_full_size(oracle_mod, config):
     oracle_mod.set_threads(oracle_mod.max_threads())
     g = gg.config_graph(config)
+    ot = oracle_mod.score(g)
     tw = assert_score_parity(oracle_mod, g)
-    assert_cluster_parity(oracle_mod, g, tw, harness.thresholds(config, tw))
+    deltas = harness.thresholds(config, tw)
+    assert_cluster_parity(oracle_mod, g, tw, deltas)
+    fused_parity(oracle_mod, g, deltas, ot)
