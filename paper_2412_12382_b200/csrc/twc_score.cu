@@ -33,7 +33,7 @@ __global__ void k0_degrees(int64_t n, const RP* __restrict__ rowptr, int* __rest
 //     filtering a sorted row keeps it sorted;
 //   * the canonical id of an upper slot p is  #upper(q < p)    (S:66-69 order);
 //   * rp_or[u] = #out(q < rowptr[u]),  eoff[u] = #upper(q < rowptr[u]);
-//   * an aligned edge (out and upper) records c2o[canonical id] = oriented slot.
+//   * so the oriented slot of an aligned edge (out and upper) is #out before its upper slot.
 // K1 is one pass over tiles of kSlotTile slots (8 consecutive slots per thread, one row search
 // per thread, then a walk) with a block scan and a decoupled look-back across tiles for the
 // two prefix counts; it also stores per-32-slot word bits and exclusive prefixes so that K1r
@@ -185,12 +185,13 @@ __global__ void __launch_bounds__(1024) k1_tile_scan(int64_t ntiles, int* __rest
 }
 
 // K1b: oriented slot = #out before p, canonical id = #upper before p (tile prefix + block
-// scan + popc); scatter col_or, record c2o for aligned edges, store the word prefixes.
+// scan + popc); scatter col_or and store the per-word prefixes (K1r and K3 derive any
+// slot's oriented / canonical index from them with one popc).
 __global__ void __launch_bounds__(kSlotThreads) k1_write(
     int64_t m2, const int* __restrict__ colidx, const unsigned* __restrict__ obits,
     const unsigned* __restrict__ ubits, const int* __restrict__ tile_out,
     const int* __restrict__ tile_up, int* __restrict__ opre, int* __restrict__ upre,
-    int* __restrict__ col_or, int* __restrict__ c2o) {
+    int* __restrict__ col_or) {
     __shared__ unsigned s_wsum[kSlotThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t ntiles = (m2 + kSlotTile - 1) / kSlotTile;
@@ -235,7 +236,6 @@ __global__ void __launch_bounds__(kSlotThreads) k1_write(
                     const unsigned below = (1u << j) - 1u;
                     const int sl = obase + __popc(ob & below);
                     col_or[sl] = v[j];
-                    if ((ub >> j) & 1u) c2o[ubase + __popc(ub & below)] = sl;
                 }
             }
         }
@@ -469,8 +469,9 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n,
 // ---------------------------------------------------------- K3 fused score epilogue
 // Edge-parallel over canonical ids; each CTA takes tiles of kTile ids, caches the tile's
 // canonical row offsets in smem and maps id -> row by binary search.  The count t of edge
-// (u,v) sits at its oriented slot: for an aligned edge (key(u) < key(v)) K1b recorded it in
-// c2o; for a reversed one it is found by binary search of u in the (short) list N+(v).
+// (u,v) sits at its oriented slot: for an aligned edge (key(u) < key(v)) that slot is the
+// number of out-slots before its upper slot (word prefix + popc); for a reversed one it is
+// found by probing the (short) list N+(v) for u.
 //   wedge = d_u + d_v - 2t - 2   (|N(u) | N(v)| - |N(u) & N(v)| - 2 for a simple graph)
 //   TW    = t - wedge            (Eq. 2)
 constexpr int kK3Threads = 256;
@@ -480,7 +481,8 @@ template <typename RP, bool BIN>
 __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int* __restrict__ deg, const int* __restrict__ eoff, const int* __restrict__ trow,
-    const int* __restrict__ rp_or, const int* __restrict__ col_or, const int* __restrict__ c2o,
+    const int* __restrict__ rp_or, const int* __restrict__ col_or,
+    const int* __restrict__ opre, const unsigned* __restrict__ obits,
     const int* __restrict__ t_or, int* __restrict__ t, int* __restrict__ wedge,
     int* __restrict__ tw, BinSpec bin) {
     constexpr int kIt = kTile / kK3Threads;
@@ -522,8 +524,11 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
             const int upu = (cached ? s_off[ri + 1] : eoff[u + 1]) - eu;
             const RP rb = rowptr[u];
             const int du = (int)(rowptr[u + 1] - rb);
-            const int v = __ldcs(colidx + rb + (RP)(du - upu) + (RP)(c - eu));  // upper slot of (u,v)
-            const int c2 = __ldcs(c2o + c);  // valid for aligned edges; issued early, used if aligned
+            const RP p = rb + (RP)(du - upu) + (RP)(c - eu);  // upper slot of (u,v)
+            const int v = __ldcs(colidx + p);
+            // oriented slot if (u,v) is aligned = #out-slots before p (word prefix + popc)
+            const int64_t wi = (int64_t)(p >> 5);
+            const int c2 = opre[wi] + __popc(obits[wi] & ((1u << (p & 31)) - 1u));
             const int dv = deg[v];
             const int ob = rp_or[v], oe = rp_or[v + 1];
             int sl;
@@ -593,7 +598,7 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
 struct ScoreWs {
     int *deg, *eoff, *rp_or, *trow, *ftrow, *tile_out, *tile_up, *opre, *upre;
     unsigned *obits, *ubits;
-    int *col_or, *t_or, *c2o, *work;
+    int *col_or, *t_or, *work;
 };
 
 static ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
@@ -613,7 +618,6 @@ static ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
     w.upre = cv.take<int>(nw);
     w.col_or = cv.take<int>(m);
     w.t_or = cv.take<int>(m);
-    w.c2o = cv.take<int>(m);
     w.work = cv.take<int>(1);
     return w;
 }
@@ -652,7 +656,7 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
                                                  w.ubits, w.tile_out, w.tile_up);
         k1_tile_scan<<<1, 1024, 0, s>>>(nst, w.tile_out, w.tile_up);
         k1_write<<<grid, kSlotThreads, 0, s>>>(m2, colidx, w.obits, w.ubits, w.tile_out,
-                                               w.tile_up, w.opre, w.upre, w.col_or, w.c2o);
+                                               w.tile_up, w.opre, w.upre, w.col_or);
         k1_rows<RP><<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, m, rowptr, w.obits, w.ubits,
                                                                    w.opre, w.upre, w.rp_or, w.eoff);
         count_launches(4);
@@ -682,12 +686,13 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         const int grid = grid_for(nt, 1, sms * 8);
         if (bin)
             k3_score<RP, true><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(m, rowptr, colidx, w.deg, w.eoff, w.trow,
-                                                           w.rp_or, w.col_or, w.c2o, w.t_or, t,
-                                                           wedge, tw, *bin);
+                                                           w.rp_or, w.col_or, w.opre, w.obits,
+                                                           w.t_or, t, wedge, tw, *bin);
         else
             k3_score<RP, false><<<grid, kK3Threads, 0, s>>>(m, rowptr, colidx, w.deg, w.eoff,
-                                                            w.trow, w.rp_or, w.col_or, w.c2o,
-                                                            w.t_or, t, wedge, tw, BinSpec{});
+                                                            w.trow, w.rp_or, w.col_or, w.opre,
+                                                            w.obits, w.t_or, t, wedge, tw,
+                                                            BinSpec{});
         count_launches(1);
         record(ev, 3, s);
     }
