@@ -130,6 +130,33 @@ twc_status twc_pipeline_host(const twc_csr *g_host, const double *deltas_host, i
                              int32_t *tw, int32_t *labels, int64_t *stats, void *stream);
 
 /* ---------------------------------------------------------------------------------------
+ * twc_similarity -- the other edge similarities of Table 1 from the triangle
+ * counts, as IEEE doubles in canonical edge order (one correctly rounded operation each):
+ *   TWC_SIM_TW        t - wedge = 3t - d_u - d_v + 2      (Eq. 2)
+ *   TWC_SIM_TECTONIC  t / (d_u + d_v)
+ *   TWC_SIM_JACCARD   t / (d_u + d_v - t)
+ *   TWC_SIM_K3        t
+ *   TWC_SIM_EFFRES    -2 / (2 + t)   (the effective-resistance upper bound 2/(2+t) of P:450,
+ *                                     negated like Table 1's -R_eff)
+ * t: device int32[m] (from twc_score); score: device double[m].  Workspace:
+ * twc_cluster_workspace_bytes(n, m, rb).  Unknown kind: TWC_EINVAL.
+ * twc_sweep_f64 -- twc_sweep on real-valued scores: keeps e iff NOT (score[e] < delta);
+ * same outputs and workspace as twc_sweep.
+ * ------------------------------------------------------------------------------------- */
+typedef enum {
+    TWC_SIM_TW = 0,
+    TWC_SIM_TECTONIC = 1,
+    TWC_SIM_JACCARD = 2,
+    TWC_SIM_K3 = 3,
+    TWC_SIM_EFFRES = 4
+} twc_sim_kind;
+twc_status twc_similarity(const twc_csr *g, const int32_t *t, int32_t kind, void *workspace,
+                          size_t workspace_bytes, double *score, void *stream);
+twc_status twc_sweep_f64(const twc_csr *g, const double *score, const double *deltas_host,
+                         int32_t k, void *workspace, size_t workspace_bytes, int32_t *labels,
+                         int64_t *stats, void *stream);
+
+/* ---------------------------------------------------------------------------------------
  * twc_validate_csr -- checks the a0 precondition: rowptr[0] = 0, rowptr
  * non-decreasing, rowptr[n] = 2m, 0 <= colidx < n, rows strictly increasing, no self-loops,
  * symmetry.  Writes a bit mask to *verdict (device int32; 0 = valid; bit 0 rowptr, bit 1 id

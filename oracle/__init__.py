@@ -9,6 +9,8 @@ this file only builds/loads it with ctypes and marshals numpy arrays.
     score(g, rows=None)          -> (t, wedge, tw)   int32[m] each, canonical (u<v lex) order
     cluster(g, tw, delta)        -> (labels int32[n], kept_edges, n_components)
     sweep(g, tw, deltas)         -> list of cluster() results
+    similarity(g, t, kind)       -> float64[m] Table-1 score (tw, tectonic, jaccard, k3, effres)
+    cluster_f64(g, score, delta) -> cluster() on real-valued scores
 
 Every function is pinned in tests/test_oracle_pins.py against brute force, closed forms,
 invariants and library routines (scipy / networkx); see DESIGN.md "Oracle pins".
@@ -48,6 +50,10 @@ def _load():
         lib.oracle_score.restype = ctypes.c_int
         lib.oracle_cluster.argtypes = [I64, P, P, P, ctypes.c_double, P, P]
         lib.oracle_cluster.restype = ctypes.c_int
+        lib.oracle_similarity.argtypes = [I64, P, P, P, ctypes.c_int32, P]
+        lib.oracle_similarity.restype = ctypes.c_int
+        lib.oracle_cluster_f64.argtypes = [I64, P, P, P, ctypes.c_double, P, P]
+        lib.oracle_cluster_f64.restype = ctypes.c_int
         lib.oracle_max_threads.restype = ctypes.c_int
         lib.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = lib
@@ -105,3 +111,32 @@ def cluster(g, tw, delta: float):
 
 def sweep(g, tw, deltas):
     return [cluster(g, tw, d) for d in deltas]
+
+
+KINDS = {"tw": 0, "tectonic": 1, "jaccard": 2, "k3": 3, "effres": 4}
+
+
+def similarity(g, t, kind):
+    """Table 1 scores (fp64) from the triangle counts t; kind in KINDS."""
+    lib = _load()
+    rowptr, colidx = _csr(g)
+    t = np.ascontiguousarray(t, dtype=np.int32)
+    out = np.zeros(t.size, dtype=np.float64)
+    if t.size:
+        rc = lib.oracle_similarity(g.n, _ptr(rowptr), _ptr(colidx), _ptr(t), KINDS[kind], _ptr(out))
+        if rc:
+            raise ValueError("bad kind")
+    return out
+
+
+def cluster_f64(g, score, delta: float):
+    lib = _load()
+    rowptr, colidx = _csr(g)
+    score = np.ascontiguousarray(score, dtype=np.float64)
+    labels = np.empty(g.n, dtype=np.int32)
+    stats = np.zeros(2, dtype=np.int64)
+    rc = lib.oracle_cluster_f64(g.n, _ptr(rowptr), _ptr(colidx), _ptr(score), float(delta),
+                                _ptr(labels), _ptr(stats))
+    if rc:
+        raise MemoryError("oracle_cluster_f64 allocation failed")
+    return labels, int(stats[0]), int(stats[1])

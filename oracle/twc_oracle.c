@@ -19,6 +19,13 @@
  *                     unlabelled vertex in ascending id order, so every vertex is labelled
  *                     with the minimum id of its component (reading C6).
  *
+ *   oracle_similarity -- the other scores of Table 1 from t and the degrees:
+ *                     Tectonic t/(d_u+d_v), Jaccard t/(d_u+d_v-t),
+ *                     K3 = t, TW = t - wedge (Eq. 2) and the effective-resistance
+ *                     proxy -2/(2+t) ("upper bound 2/(2+t)", negated as Table 1's
+ *                     -R_eff); one IEEE double operation per score.
+ *   oracle_cluster_f64 -- Alg. 1 on real-valued scores: keep e iff NOT (sim(e) < delta).
+ *
  * Parallelism: the only parallelism is an OpenMP loop over rows in oracle_score (disjoint
  * writes, deterministic).  Everything is int32/int64 integer arithmetic, so there is no
  * rounding anywhere (reading C18).  The comparison (double)TW < delta is exact (|TW| < 2^53).
@@ -160,3 +167,48 @@ int oracle_cluster(int64_t n, const int64_t *rowptr, const int32_t *colidx,
     free(kdeg); free(fill); free(kadj); free(queue);
     return 0;
 }
+
+/* Degree-based scores of Table 1 for every canonical edge, in the same order as
+ * oracle_score; kind: 0 TW, 1 Tectonic, 2 Jaccard, 3 K3, 4 effective-resistance proxy. */
+int oracle_similarity(int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                      const int32_t *t, int32_t kind, double *out) {
+    int64_t c = 0;
+    for (int64_t u = 0; u < n; ++u) {
+        const int64_t du = rowptr[u + 1] - rowptr[u];
+        for (int64_t p = rowptr[u]; p < rowptr[u + 1]; ++p) {
+            const int64_t v = colidx[p];
+            if (v <= u) continue;
+            const int64_t dv = rowptr[v + 1] - rowptr[v];
+            const double tt = (double)t[c];
+            double x;
+            switch (kind) {
+                case 0: x = (double)(t[c] - (du + dv - 2 * (int64_t)t[c] - 2)); break;
+                case 1: x = tt / (double)(du + dv); break;
+                case 2: x = tt / (double)(du + dv - t[c]); break;
+                case 3: x = tt; break;
+                case 4: x = -2.0 / (2.0 + tt); break;
+                default: return 1;
+            }
+            out[c++] = x;
+        }
+    }
+    return 0;
+}
+
+/* Alg. 1 on real-valued scores (same contract as oracle_cluster). */
+int oracle_cluster_f64(int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                       const double *score, double delta, int32_t *labels, int64_t *stats) {
+    if (n <= 0) {
+        if (stats) { stats[0] = 0; stats[1] = 0; }
+        return 0;
+    }
+    int64_t m = rowptr[n] / 2;
+    /* map the real-valued keep decision onto a 0/1 integer score and reuse oracle_cluster */
+    int32_t *keep = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m + 1));
+    if (!keep) return 1;
+    for (int64_t c = 0; c < m; ++c) keep[c] = (score[c] < delta) ? 0 : 1;
+    int rc = oracle_cluster(n, rowptr, colidx, keep, 0.5, labels, stats);
+    free(keep);
+    return rc;
+}
+

@@ -73,6 +73,8 @@ def load_library(path: str = LIB_PATH):
         "twc_kernel_launches": (I64, []),
         "twc_score_sweep_workspace_bytes": (SZ, [I64, I64, I32]),
         "twc_score_sweep": (ctypes.c_int, [CP, P, I32, P, SZ, P, P, P, P, P, P, P]),
+        "twc_similarity": (ctypes.c_int, [CP, P, I32, P, SZ, P, P]),
+        "twc_sweep_f64": (ctypes.c_int, [CP, P, P, I32, P, SZ, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -234,6 +236,42 @@ def twc_score_sweep(rowptr, colidx, deltas, out=None, labels=None, stats=None, w
                                ws.numel(), _ptr(t), _ptr(wedge), _ptr(tw), _ptr(labels),
                                _ptr(stats), _stream(stream), ev[0] if ev else None))
     return t, wedge, tw, labels, stats
+
+
+SIM_KINDS = {"tw": 0, "tectonic": 1, "jaccard": 2, "k3": 3, "effres": 4}
+
+
+def twc_similarity(rowptr, colidx, t, kind, out=None, workspace=None, stream=None):
+    """Table-1 edge similarity (fp64, canonical order) from the triangle counts t:
+    kind in 'tw', 'tectonic', 'jaccard', 'k3', 'effres' (P:405-423, P:450)."""
+    lib = load_library()
+    g, n, m = _graph(rowptr, colidx)
+    dev = colidx.device
+    if out is None:
+        out = torch.empty(m, dtype=torch.float64, device=dev)
+    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    _check(lib.twc_similarity(ctypes.byref(g), _ptr(t), SIM_KINDS[kind], _ptr(ws), ws.numel(),
+                              _ptr(out), _stream(stream)))
+    return out
+
+
+def twc_sweep_f64(rowptr, colidx, score, deltas, labels=None, stats=None, workspace=None,
+                  stream=None):
+    """Alg. 1 for k thresholds on real-valued scores: keep e iff NOT (score[e] < delta)."""
+    lib = load_library()
+    g, n, m = _graph(rowptr, colidx)
+    dev = colidx.device
+    deltas = [float(d) for d in deltas]
+    k = len(deltas)
+    if labels is None:
+        labels = torch.empty((k, n), dtype=torch.int32, device=dev)
+    if stats is None:
+        stats = torch.empty((k, 2), dtype=torch.int64, device=dev)
+    arr = (ctypes.c_double * k)(*deltas)
+    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    _check(lib.twc_sweep_f64(ctypes.byref(g), _ptr(score), ctypes.cast(arr, ctypes.c_void_p), k,
+                             _ptr(ws), ws.numel(), _ptr(labels), _ptr(stats), _stream(stream)))
+    return labels, stats
 
 
 def twc_pipeline_host(rowptr, colidx, deltas, want_scores=True, out=None, workspace=None,

@@ -239,6 +239,54 @@ twc_status twc_score_sweep(const twc_csr* g, const double* deltas_host, int32_t 
     return cuda_status(e, "twc_score_sweep");
 }
 
+twc_status twc_similarity(const twc_csr* g, const int32_t* t, int32_t kind, void* ws,
+                          size_t ws_bytes, double* score, void* stream) {
+    g_err.clear();
+    twc_status st = check_csr(g);
+    if (st) return st;
+    if (kind < TWC_SIM_TW || kind > TWC_SIM_EFFRES) return fail(TWC_EINVAL, "unknown kind %d", kind);
+    if (g->m > 0 && (!t || !score)) return fail(TWC_EINVAL, "t or score is NULL");
+    if (g->m == 0) return TWC_OK;
+    st = check_ws(ws, ws_bytes, cluster_ws_bytes(g->n, g->m));
+    if (st) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (g->rowptr_bytes == 4)
+        e = similarity_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx, t,
+                                 kind, ws, ws_bytes, score, s);
+    else
+        e = similarity_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr),
+                                       g->colidx, t, kind, ws, ws_bytes, score, s);
+    return cuda_status(e, "twc_similarity");
+}
+
+twc_status twc_sweep_f64(const twc_csr* g, const double* score, const double* deltas_host,
+                         int32_t k, void* ws, size_t ws_bytes, int32_t* labels, int64_t* stats,
+                         void* stream) {
+    g_err.clear();
+    twc_status st = check_csr(g);
+    if (st) return st;
+    if (k < 1 || k > 1024) return fail(TWC_EINVAL, "k=%d must be in [1, 1024]", k);
+    if (!deltas_host) return fail(TWC_EINVAL, "deltas_host is NULL");
+    for (int i = 0; i < k; ++i)
+        if (isnan(deltas_host[i])) return fail(TWC_EINVAL, "delta is NaN");
+    if (g->n > 0 && !labels) return fail(TWC_EINVAL, "labels is NULL");
+    if (g->m > 0 && !score) return fail(TWC_EINVAL, "score is NULL");
+    st = check_ws(ws, ws_bytes, cluster_ws_bytes(g->n, g->m));
+    if (st) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (g->rowptr_bytes == 4)
+        e = sweep_f64_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx, score,
+                                deltas_host, k, ws, ws_bytes, labels,
+                                reinterpret_cast<long long*>(stats), s);
+    else
+        e = sweep_f64_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr),
+                                      g->colidx, score, deltas_host, k, ws, ws_bytes, labels,
+                                      reinterpret_cast<long long*>(stats), s);
+    return cuda_status(e, "twc_sweep_f64");
+}
+
 // ---- end-to-end from host buffers --------------------------------------------------------
 struct PipeWs {
     void* rowptr;

@@ -16,6 +16,7 @@
 // keeps it (its "band": thr_i <= TW < thr_{i-1}); step i then hooks only band i's edges and
 // snapshots the compressed labels.
 #include <algorithm>
+#include <cstring>
 
 #include "twc_common.cuh"
 #include "twc_internal.h"
@@ -79,10 +80,11 @@ constexpr int kItemsPerThread = kTile / kSweepThreads;  // 4
 constexpr int kMaxTileRows = 2048;
 
 // Pass 1: histogram of bands (edges kept at no threshold are not counted).
-__global__ void __launch_bounds__(kSweepThreads) k_band_count(int64_t m, const int* __restrict__ tw,
-                                                              const long long* __restrict__ thr_g,
+template <typename S, typename TH>
+__global__ void __launch_bounds__(kSweepThreads) k_band_count(int64_t m, const S* __restrict__ tw,
+                                                              const TH* __restrict__ thr_g,
                                                               int k, int* __restrict__ cnt) {
-    __shared__ long long s_thr[kMaxK];
+    __shared__ TH s_thr[kMaxK];
     __shared__ int s_hist[kMaxK];
     for (int i = threadIdx.x; i < k; i += blockDim.x) {
         s_thr[i] = thr_g[i];
@@ -91,7 +93,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_band_count(int64_t m, const i
     __syncthreads();
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m;
          c += (int64_t)gridDim.x * blockDim.x) {
-        const int b = band_of(tw[c], s_thr, k);
+        const int b = band_of_t(tw[c], s_thr, k);
         if (b < k) atomicAdd(&s_hist[b], 1);
     }
     __syncthreads();
@@ -118,13 +120,13 @@ __global__ void k_band_offsets(const int* __restrict__ cnt, int k, const int* __
 // Pass 2: scatter each kept edge (u, v) into its band's segment.  Each CTA reserves, per band,
 // one contiguous range per tile (one global atomic per band and tile).  A thread handles
 // kItemsPerThread consecutive canonical ids: one row search, then a walk along the rows.
-template <typename RP>
+template <typename RP, typename S, typename TH>
 __global__ void __launch_bounds__(kSweepThreads) k_band_scatter(
     int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
-    const int* __restrict__ eoff, const int* __restrict__ trow, const int* __restrict__ tw,
-    const long long* __restrict__ thr_g, int k, int* __restrict__ cursor,
+    const int* __restrict__ eoff, const int* __restrict__ trow, const S* __restrict__ tw,
+    const TH* __restrict__ thr_g, int k, int* __restrict__ cursor,
     int2* __restrict__ pairs) {
-    __shared__ long long s_thr[kMaxK];
+    __shared__ TH s_thr[kMaxK];
     __shared__ int s_cnt[kMaxK];
     __shared__ int s_off[kMaxTileRows + 1];
     for (int i = threadIdx.x; i < k; i += blockDim.x) s_thr[i] = thr_g[i];
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_band_scatter(
             band[it] = k;
             rank[it] = 0;
             if (c < c1) {
-                band[it] = band_of(tw[c], s_thr, k);
+                band[it] = band_of_t(tw[c], s_thr, k);
                 if (band[it] < k) {
                     rank[it] = atomicAdd(&s_cnt[band[it]], 1);
                     any = true;
@@ -279,6 +281,21 @@ void sweep_plan(const long long* thr, int k, SweepPlan* P) {
             int tmp = P->order[j]; P->order[j] = P->order[j - 1]; P->order[j - 1] = tmp;
         }
     for (int i = 0; i < k; ++i) P->thr[i] = thr[P->order[i]];
+    for (int i = 0; i < k; ++i) P->fresh[i] = (i == 0) || (P->thr[i] < P->thr[i - 1]);
+}
+
+void sweep_plan_f64(const double* thr, int k, SweepPlan* P) {
+    P->k = k;
+    for (int i = 0; i < k; ++i) P->order[i] = i;
+    for (int i = 1; i < k; ++i)
+        for (int j = i; j > 0 && thr[P->order[j]] > thr[P->order[j - 1]]; --j) {
+            int tmp = P->order[j]; P->order[j] = P->order[j - 1]; P->order[j - 1] = tmp;
+        }
+    for (int i = 0; i < k; ++i) {
+        const double d = thr[P->order[i]];
+        memcpy(&P->thr[i], &d, sizeof(double));  // bit pattern, uploaded as is
+        P->fresh[i] = (i == 0) || (d < thr[P->order[i - 1]]);
+    }
 }
 
 void sweep_upload(const SweepPlan& P, long long* thr_dev, int* order_dev, cudaStream_t s) {
@@ -355,7 +372,7 @@ void sweep_loop(int64_t n, int64_t m, const SweepPlan& P, const int2* pairs, con
     const int fin_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
     for (int i = 0; i < P.k; ++i) {
         const int idx = P.order[i];
-        if (m > 0 && (i == 0 || P.thr[i] < P.thr[i - 1])) {
+        if (m > 0 && P.fresh[i]) {
             k_hook_list<<<hook_grid, 256, 0, s>>>(pairs, off, i, parent);
             count_launches(1);
         }
@@ -390,13 +407,13 @@ cudaError_t sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         tile_first_rows(w.eoff, (int)n, m, w.trow, s);
         const int cgrid = (int)std::min<int64_t>((m + kSweepThreads - 1) / kSweepThreads,
                                                  (int64_t)sms * 8);
-        k_band_count<<<cgrid, kSweepThreads, 0, s>>>(m, tw, w.thr, k, w.cnt);
+        k_band_count<int, long long><<<cgrid, kSweepThreads, 0, s>>>(m, tw, w.thr, k, w.cnt);
         count_launches(1);
         band_offsets(w.cnt, k, w.order, w.off, w.cursor, st, s);
         const int64_t nt = num_tiles(m);
         const int sgrid = (int)std::min<int64_t>(nt, (int64_t)sms * 8);
-        k_band_scatter<RP><<<sgrid, kSweepThreads, 0, s>>>(m, rowptr, colidx, w.eoff, w.trow, tw,
-                                                           w.thr, k, w.cursor, w.pairs);
+        k_band_scatter<RP, int, long long><<<sgrid, kSweepThreads, 0, s>>>(
+            m, rowptr, colidx, w.eoff, w.trow, tw, w.thr, k, w.cursor, w.pairs);
         count_launches(1);
     }
     record(ev, 1, s);
@@ -488,6 +505,51 @@ template cudaError_t sweep_impl<int>(int64_t, int64_t, const int*, const int*, c
 template cudaError_t sweep_impl<long long>(int64_t, int64_t, const long long*, const int*,
                                            const int*, const long long*, int, void*, size_t,
                                            int*, long long*, cudaStream_t, cudaEvent_t*);
+
+// ------------------------------------------------------------------ sweep on fp64 scores
+// Alg. 1 for any Table-1 score: keep e iff NOT (score(e) < delta) in IEEE double;
+// identical band / union-find machinery with double thresholds.
+template <typename RP>
+cudaError_t sweep_f64_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+                           const double* score, const double* deltas, int k, void* ws,
+                           size_t ws_bytes, int* labels, long long* stats, cudaStream_t s) {
+    Carver cv(ws, ws_bytes);
+    ClusterWs w = carve_cluster(cv, n, m);
+    unsigned long long* st = stats ? reinterpret_cast<unsigned long long*>(stats) : w.stats;
+    cudaMemsetAsync(st, 0, sizeof(long long) * 2 * (size_t)k, s);
+    if (n == 0) return cudaGetLastError();
+    const int sms = num_sms();
+    SweepPlan P;
+    sweep_plan_f64(deltas, k, &P);
+    sweep_upload(P, w.thr, w.order, s);  // bit patterns of the doubles
+    const double* thr_d = reinterpret_cast<const double*>(w.thr);
+    cudaMemsetAsync(w.cnt, 0, sizeof(int) * (k + 1), s);
+    init_parent(n, w.parent, s);
+    if (m > 0) {
+        upper_counts<RP>(n, rowptr, colidx, w.up, s);
+        exclusive_scan(w.up, w.eoff, n, w.scan_tmp, s);
+        tile_first_rows(w.eoff, (int)n, m, w.trow, s);
+        const int cgrid = (int)std::min<int64_t>((m + kSweepThreads - 1) / kSweepThreads,
+                                                 (int64_t)sms * 8);
+        k_band_count<double, double><<<cgrid, kSweepThreads, 0, s>>>(m, score, thr_d, k, w.cnt);
+        count_launches(1);
+        band_offsets(w.cnt, k, w.order, w.off, w.cursor, st, s);
+        const int64_t nt = num_tiles(m);
+        const int sgrid = (int)std::min<int64_t>(nt, (int64_t)sms * 8);
+        k_band_scatter<RP, double, double><<<sgrid, kSweepThreads, 0, s>>>(
+            m, rowptr, colidx, w.eoff, w.trow, score, thr_d, k, w.cursor, w.pairs);
+        count_launches(1);
+    }
+    sweep_loop(n, m, P, w.pairs, w.off, w.parent, labels, st, s);
+    return cudaGetLastError();
+}
+
+template cudaError_t sweep_f64_impl<int>(int64_t, int64_t, const int*, const int*, const double*,
+                                         const double*, int, void*, size_t, int*, long long*,
+                                         cudaStream_t);
+template cudaError_t sweep_f64_impl<long long>(int64_t, int64_t, const long long*, const int*,
+                                               const double*, const double*, int, void*, size_t,
+                                               int*, long long*, cudaStream_t);
 
 // ------------------------------------------------------------------------ validation
 template <typename RP>

@@ -98,4 +98,16 @@ __device__ __forceinline__ int band_of(long long val, const long long* thr, int 
     return lo;
 }
 
+// Same for any score / threshold type (int32 TW with int64 thresholds, fp64 scores with fp64
+// thresholds): b = #{i : thr[i] > val}.
+template <typename V, typename T>
+__device__ __forceinline__ int band_of_t(V val, const T* thr, int k) {
+    int lo = 0, hi = k;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (thr[mid] > (T)val) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
 }  // namespace twc

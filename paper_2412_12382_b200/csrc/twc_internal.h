@@ -54,9 +54,11 @@ constexpr int kMaxK = 1024;  // thresholds per sweep
 struct SweepPlan {           // thresholds sorted descending (fewest kept edges first)
     int k;
     int order[kMaxK];        // caller index of the i-th threshold
-    long long thr[kMaxK];    // keep iff TW >= thr[i]
+    long long thr[kMaxK];    // keep iff TW >= thr[i] (fp64 sweeps: the double's bit pattern)
+    bool fresh[kMaxK];       // thr[i] differs from thr[i-1] (step i has its own band)
 };
 void sweep_plan(const long long* thr, int k, SweepPlan* P);
+void sweep_plan_f64(const double* thr, int k, SweepPlan* P);
 void sweep_upload(const SweepPlan& P, long long* thr_dev, int* order_dev, cudaStream_t s);
 void band_offsets(const int* cnt, int k, const int* order_dev, int* off, int* cursor,
                   unsigned long long* stats, cudaStream_t s);
@@ -95,6 +97,16 @@ template <typename RP>
 cudaError_t sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, const int* tw,
                        const long long* thr, int k, void* ws, size_t ws_bytes, int* labels,
                        long long* stats, cudaStream_t s, cudaEvent_t* ev = nullptr);
+
+// ---- real-valued scores (twc_similarity.cu / twc_cluster.cu) --------------------------------
+template <typename RP>
+cudaError_t similarity_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+                            const int* t, int kind, void* ws, size_t ws_bytes, double* out,
+                            cudaStream_t s);
+template <typename RP>
+cudaError_t sweep_f64_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+                           const double* score, const double* deltas, int k, void* ws,
+                           size_t ws_bytes, int* labels, long long* stats, cudaStream_t s);
 
 // ---- validation (twc_cluster.cu) -----------------------------------------------------------
 template <typename RP>

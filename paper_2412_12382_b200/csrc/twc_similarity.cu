@@ -1,0 +1,88 @@
+// twc_similarity.cu -- the other edge similarities of Table 1 from the triangle
+// counts, in fp64, canonical edge order.
+//
+//   kind 0  TW        t - wedge = 3t - d_u - d_v + 2          (Eq. 2)
+//   kind 1  Tectonic  t / (d_u + d_v)
+//   kind 2  Jaccard   t / (d_u + d_v - t)
+//   kind 3  K3        t
+//   kind 4  -R_eff proxy  -2 / (2 + t)                         (P:450 upper bound 2/(2+t),
+//                                                               negated as Table 1's -R_eff)
+// Each score is one IEEE double operation on exact integers, so it is correctly rounded and
+// bit-identical to any other correctly rounded evaluation (reading C18).
+#include <algorithm>
+
+#include "twc_common.cuh"
+#include "twc_internal.h"
+
+namespace twc {
+
+constexpr int kSimThreads = 256;
+constexpr int kSimTileRows = 2048;
+
+template <typename RP>
+__global__ void __launch_bounds__(kSimThreads) k_similarity(
+    int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
+    const int* __restrict__ eoff, const int* __restrict__ trow, const int* __restrict__ t,
+    int kind, double* __restrict__ out) {
+    __shared__ int s_off[kSimTileRows + 1];
+    const int64_t ntiles = num_tiles(m);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int c0 = (int)(tile * kTile);
+        const int c1 = (int)min((int64_t)c0 + kTile, m);
+        const int r0 = trow[tile];
+        const int nr = trow[tile + 1] - r0 + 1;
+        const bool cached = nr <= kSimTileRows;
+        __syncthreads();
+        if (cached)
+            for (int i = threadIdx.x; i <= nr; i += blockDim.x) s_off[i] = eoff[r0 + i];
+        __syncthreads();
+        for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+            const int ri = cached ? last_le(s_off, nr + 1, c) : last_le(eoff + r0, nr + 1, c);
+            const int u = r0 + ri;
+            const int eu = cached ? s_off[ri] : eoff[u];
+            const int upu = (cached ? s_off[ri + 1] : eoff[u + 1]) - eu;
+            const RP rb = rowptr[u];
+            const long long du = (long long)(rowptr[u + 1] - rb);
+            const int v = colidx[rb + (RP)(du - upu) + (RP)(c - eu)];
+            const long long dv = (long long)(rowptr[v + 1] - rowptr[v]);
+            const long long tt = t[c];
+            double x;
+            switch (kind) {
+                case 0: x = (double)(3 * tt - du - dv + 2); break;
+                case 1: x = (double)tt / (double)(du + dv); break;
+                case 2: x = (double)tt / (double)(du + dv - tt); break;
+                case 3: x = (double)tt; break;
+                default: x = -2.0 / (2.0 + (double)tt); break;
+            }
+            out[c] = x;
+        }
+    }
+}
+
+template <typename RP>
+cudaError_t similarity_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+                            const int* t, int kind, void* ws, size_t ws_bytes, double* out,
+                            cudaStream_t s) {
+    if (m == 0 || n == 0) return cudaGetLastError();
+    // reuse the cluster workspace layout for the canonical offsets: up, eoff, scan, tile rows
+    Carver cv(ws, ws_bytes);
+    int* up = cv.take<int>(n);
+    int* eoff = cv.take<int>(n + 1);
+    int* scan_tmp = cv.take<int>(scan_temp_bytes(n) / sizeof(int));
+    int* trow = cv.take<int>(num_tiles(m) + 1);
+    upper_counts<RP>(n, rowptr, colidx, up, s);
+    exclusive_scan(up, eoff, n, scan_tmp, s);
+    tile_first_rows(eoff, (int)n, m, trow, s);
+    const int grid = (int)std::min<int64_t>(num_tiles(m), (int64_t)num_sms() * 8);
+    k_similarity<RP><<<grid, kSimThreads, 0, s>>>(m, rowptr, colidx, eoff, trow, t, kind, out);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+template cudaError_t similarity_impl<int>(int64_t, int64_t, const int*, const int*, const int*,
+                                          int, void*, size_t, double*, cudaStream_t);
+template cudaError_t similarity_impl<long long>(int64_t, int64_t, const long long*, const int*,
+                                                const int*, int, void*, size_t, double*,
+                                                cudaStream_t);
+
+}  // namespace twc
