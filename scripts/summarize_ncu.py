@@ -88,8 +88,14 @@ def launch_summary(tag, path):
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     seq = [(r[ki].split("(")[0].replace("void ", ""), float(r[vi].replace(",", "")))
            for r in data if len(r) > vi]
-    idx = [k for k, (nm, _) in enumerate(seq) if "k0_degrees" in nm]
-    last = [x for x in seq[idx[-1]:] if not x[0].startswith("at::")]
+    idx = [k for k, (nm, _) in enumerate(seq) if "k0_degrees" in nm] + [len(seq)]
+    # the last complete fused step (twc_score_sweep: contains k_band_place)
+    steps = [seq[a:b] for a, b in zip(idx[:-1], idx[1:])]
+    fused = [st for st in steps if any("k_band_place" in nm for nm, _ in st)]
+    chosen = fused[-1] if fused else steps[-1]
+    # a fused step ends at its last k_finalize (the separate calls may follow in the same chunk)
+    last_fin = max((k for k, (nm, _) in enumerate(chosen) if "k_finalize" in nm), default=len(chosen) - 1)
+    last = [x for x in chosen[:last_fin + 1] if not x[0].startswith("at::")]
     tot = sum(v for _, v in last)
     agg, cnt = OrderedDict(), OrderedDict()
     for nm, v in last:
@@ -98,7 +104,7 @@ def launch_summary(tag, path):
     lines = [f"# Launch list of one bench step ({tag})", "",
              "`ncu --metrics gpu__time_duration.sum --clock-control none` over "
              "`python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline` (config 5); the "
-             "last complete step.  ncu serialises launches and starts each cold, so the SHARES "
+             "last complete fused step (`twc_score_sweep`).  ncu serialises launches and starts each cold, so the SHARES "
              "are what compare with bench.py's live phase timings, not the absolute times.", "",
              "| kernel | launches | device time (us) | share |", "|---|---|---|---|"]
     for nm, v in agg.items():
