@@ -11,6 +11,9 @@ this file only builds/loads it with ctypes and marshals numpy arrays.
     sweep(g, tw, deltas)         -> list of cluster() results
     similarity(g, t, kind)       -> float64[m] Table-1 score (tw, tectonic, jaccard, k3, effres)
     cluster_f64(g, score, delta) -> cluster() on real-valued scores
+    partition_stats(g, labels)   -> (n_communities, largest, intra_edges, sum_D2, modularity)
+    sweep_report(g, tw, deltas)  -> per-delta points (kept, #CC, largest, E_in, sum_D2, Q)
+    select(deltas, largest, n, modularity, jump_factor=0.1) -> (index, rule)
 
 Every function is pinned in tests/test_oracle_pins.py against brute force, closed forms,
 invariants and library routines (scipy / networkx); see DESIGN.md "Oracle pins".
@@ -54,6 +57,10 @@ def _load():
         lib.oracle_similarity.restype = ctypes.c_int
         lib.oracle_cluster_f64.argtypes = [I64, P, P, P, ctypes.c_double, P, P]
         lib.oracle_cluster_f64.restype = ctypes.c_int
+        lib.oracle_partition_stats.argtypes = [I64, P, P, P, P, P]
+        lib.oracle_partition_stats.restype = ctypes.c_int
+        lib.oracle_select.argtypes = [ctypes.c_int32, P, P, I64, P, ctypes.c_double, P]
+        lib.oracle_select.restype = ctypes.c_int32
         lib.oracle_max_threads.restype = ctypes.c_int
         lib.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = lib
@@ -140,3 +147,43 @@ def cluster_f64(g, score, delta: float):
     if rc:
         raise MemoryError("oracle_cluster_f64 allocation failed")
     return labels, int(stats[0]), int(stats[1])
+
+
+def partition_stats(g, labels):
+    """(n_communities, largest, intra_edges, sum_c D_c^2, modularity) of labels[n]."""
+    lib = _load()
+    rowptr, colidx = _csr(g)
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    out = np.zeros(4, dtype=np.int64)
+    q = np.zeros(1, dtype=np.float64)
+    rc = lib.oracle_partition_stats(g.n, _ptr(rowptr), _ptr(colidx), _ptr(labels), _ptr(out),
+                                    _ptr(q))
+    if rc == 1:
+        raise MemoryError("oracle_partition_stats allocation failed")
+    if rc == 2:
+        raise ValueError("label out of range")
+    return int(out[0]), int(out[1]), int(out[2]), int(out[3]), float(q[0])
+
+
+def select(deltas, largest, n, modularity, jump_factor=0.1):
+    """Selection rules of P:898-900 -> (index into deltas, rule 0 = jump / 1 = modularity)."""
+    lib = _load()
+    d = np.ascontiguousarray(deltas, dtype=np.float64)
+    lg = np.ascontiguousarray(largest, dtype=np.int64)
+    q = np.ascontiguousarray(modularity, dtype=np.float64)
+    rule = np.zeros(1, dtype=np.int32)
+    idx = lib.oracle_select(int(d.size), _ptr(d), _ptr(lg), int(n), _ptr(q), float(jump_factor),
+                            _ptr(rule))
+    return int(idx), int(rule[0])
+
+
+def sweep_report(g, tw, deltas):
+    """One dict per delta (input order): kept, n_cc, largest, intra, sum_d2, modularity."""
+    pts = []
+    for d in deltas:
+        labels, kept, ncc = cluster(g, tw, d)
+        nc, largest, intra, sd2, q = partition_stats(g, labels)
+        assert nc == ncc
+        pts.append({"delta": float(d), "kept": kept, "n_cc": nc, "largest": largest,
+                    "intra": intra, "sum_d2": sd2, "modularity": q})
+    return pts

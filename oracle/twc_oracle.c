@@ -26,6 +26,20 @@
  *                     -R_eff); one IEEE double operation per score.
  *   oracle_cluster_f64 -- Alg. 1 on real-valued scores: keep e iff NOT (sim(e) < delta).
  *
+ *   oracle_partition_stats -- the statistics of one partition that the threshold-selection
+ *                     study plots: number of components, size of the
+ *                     largest, and the modularity
+ *                       Q = (1/2m) sum_{u,v} (A_uv - d_u d_v / 2m) [c_u = c_v]
+ *                     evaluated from two exact integers (reading C21): the ordered-pair sum of
+ *                     A_uv over same-community pairs is 2 E_in (E_in = edges with both ends in
+ *                     one community) and the sum of d_u d_v over them is sum_c D_c^2 (D_c = total
+ *                     degree of community c), so Q = (4 m E_in - sum_c D_c^2) / (4 m^2), one
+ *                     IEEE division of two exactly represented integers.
+ *   oracle_select  -- the two rules of thumb of P:898-900 (reading C22): on the
+ *                     decreasing-delta scan, the largest single-step increase of the normalised
+ *                     largest-component size; if it is >= jump_factor return the higher delta
+ *                     of that step, else the delta of maximum modularity (ties -> larger delta).
+ *
  * Parallelism: the only parallelism is an OpenMP loop over rows in oracle_score (disjoint
  * writes, deterministic).  Everything is int32/int64 integer arithmetic, so there is no
  * rounding anywhere (reading C18).  The comparison (double)TW < delta is exact (|TW| < 2^53).
@@ -212,3 +226,73 @@ int oracle_cluster_f64(int64_t n, const int64_t *rowptr, const int32_t *colidx,
     return rc;
 }
 
+
+/*
+ * Statistics of the partition labels[n] (labels[u] in [0, n) names u's community; the labels
+ * of a connected-components run are its minimum vertex ids).
+ * out[4] = {number of communities, size of the largest, E_in, sum_c D_c^2};
+ * *q = modularity or NaN when m = 0 ("undefined marker").
+ * Returns 0, 1 on allocation failure, 2 when a label is out of range.
+ */
+int oracle_partition_stats(int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                           const int32_t *labels, int64_t *out, double *q) {
+    out[0] = out[1] = out[2] = out[3] = 0;
+    int64_t m = n > 0 ? rowptr[n] / 2 : 0;
+    if (n <= 0) { *q = 0.0 / 0.0; return 0; }
+    int64_t *size = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    int64_t *dsum = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    if (!size || !dsum) { free(size); free(dsum); return 1; }
+    for (int64_t u = 0; u < n; ++u) {
+        if (labels[u] < 0 || labels[u] >= n) { free(size); free(dsum); return 2; }
+        size[labels[u]] += 1;
+        dsum[labels[u]] += rowptr[u + 1] - rowptr[u];          /* D_c = sum of degrees */
+    }
+    for (int64_t c = 0; c < n; ++c) {
+        if (size[c] == 0) continue;
+        out[0] += 1;                                            /* communities */
+        if (size[c] > out[1]) out[1] = size[c];                 /* largest */
+        out[3] += dsum[c] * dsum[c];                            /* sum_c D_c^2 */
+    }
+    for (int64_t u = 0; u < n; ++u)                             /* E_in: each edge once (u<v) */
+        for (int64_t p = rowptr[u]; p < rowptr[u + 1]; ++p)
+            if (colidx[p] > u && labels[colidx[p]] == labels[u]) out[2] += 1;
+    if (m == 0) *q = 0.0 / 0.0;
+    else *q = (double)(4 * m * out[2] - out[3]) / (double)(4 * m * m);
+    free(size); free(dsum);
+    return 0;
+}
+
+/*
+ * The selection rules over k sweep points: deltas[k] (any order), largest[k] = size
+ * of the largest community at deltas[i], modularity[k].  Returns the index of the selected
+ * point and sets *rule = 0 (largest-component jump) or 1 (maximum modularity).  The
+ * normalised increase of one step is (double)(largest_lower - largest_higher) / (double)n.
+ */
+int32_t oracle_select(int32_t k, const double *deltas, const int64_t *largest, int64_t n,
+                      const double *modularity, double jump_factor, int32_t *rule) {
+    /* indices by decreasing delta (insertion sort; equal deltas keep input order) */
+    int32_t *ord = (int32_t *)malloc(sizeof(int32_t) * (size_t)(k > 0 ? k : 1));
+    if (!ord || k <= 0) { free(ord); *rule = -1; return -1; }
+    for (int32_t i = 0; i < k; ++i) {
+        int32_t j = i;
+        while (j > 0 && deltas[ord[j - 1]] < deltas[i]) { ord[j] = ord[j - 1]; --j; }
+        ord[j] = i;
+    }
+    /* rule 1: "a sudden increment in the size of the largest community" on decreasing delta */
+    int32_t best = -1;
+    double best_inc = 0.0;
+    for (int32_t i = 0; i + 1 < k; ++i) {
+        double inc = (double)(largest[ord[i + 1]] - largest[ord[i]]) / (double)n;
+        if (best < 0 || inc > best_inc) { best = ord[i]; best_inc = inc; }
+    }
+    if (best >= 0 && best_inc >= jump_factor) { *rule = 0; free(ord); return best; }
+    /* rule 2: "picking a threshold that maximizes the modularity", ties -> larger delta */
+    best = ord[0];
+    for (int32_t i = 1; i < k; ++i) {
+        double a = modularity[ord[i]], b = modularity[best];
+        if (a == a && (b != b || a > b)) best = ord[i];
+    }
+    *rule = 1;
+    free(ord);
+    return best;
+}
