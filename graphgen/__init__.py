@@ -171,10 +171,24 @@ def bridge_triangles() -> Graph:
 # ---------------------------------------------------------------------------------------
 
 def erdos_renyi(n: int, p: float, seed: int) -> Graph:
+    """G(n, p) by one Bernoulli draw per vertex pair: O(n^2) memory, so small n only."""
+    if n > 20_000:
+        raise ValueError("erdos_renyi enumerates all pairs; use gnm() for large n")
     rng = np.random.default_rng(seed)
     a, b = np.triu_indices(n, 1)
     keep = rng.random(a.size) < p
     return csr_from_pairs(n, a[keep], b[keep], meta={"kind": "er", "n": n, "p": p, "seed": seed})
+
+
+def gnm(n: int, m: int, seed: int, rowptr_dtype=np.int32) -> Graph:
+    """Sparse uniform random graph for large n: m uniformly drawn vertex pairs, loops and
+    duplicates dropped (so the realised m is slightly below the request)."""
+    rng = np.random.default_rng(seed)
+    a = rng.integers(0, n, size=m, dtype=np.int64)
+    b = rng.integers(0, n, size=m, dtype=np.int64)
+    keep = a != b
+    return csr_from_pairs(n, a[keep], b[keep], rowptr_dtype=rowptr_dtype,
+                          meta={"kind": "gnm", "n": n, "m": m, "seed": seed})
 
 
 def two_block_sbm(n: int, p1: float, p2: float, q: float, seed: int) -> Graph:

@@ -157,6 +157,48 @@ twc_status twc_sweep_f64(const twc_csr *g, const double *score, const double *de
                          int64_t *stats, void *stream);
 
 /* ---------------------------------------------------------------------------------------
+ * twc_partition_stats -- the statistics the threshold-selection study plots for each
+ * partition ("norm # CC ... norm |largest CC|", modularity P:350-352; S:346;
+ * SURVEY 8(f) NEXT(2)), for k partitions of the INPUT graph g at once.
+ *   labels:     device int32[k*n]; labels[j*n + u] in [0, n) names u's community in
+ *               partition j (the min-id labels of twc_sweep qualify; any labelling works).
+ *   counts:     device int64[4k]; counts[4j + 0] = number of communities, [4j + 1] = size of the
+ *               largest, [4j + 2] = E_in, the number of edges of g inside one community,
+ *               [4j + 3] = sum over communities c of D_c^2, D_c = sum of deg(u), u in c.
+ *   modularity: device double[k] or NULL; modularity[j] = (4 m E_in - sum D_c^2) / (4 m^2),
+ *               one IEEE division of exact integers (reading C21; P:350-352's double sum over
+ *               ordered pairs), NaN when m = 0.
+ * The norm statistics of P:888 are counts / n and kept edges (twc_sweep stats) / m.
+ * Synchronises `stream` (a device flag is read back).  TWC_EINVAL: k outside [1, 1024],
+ * m > 1.5e9 (4m^2 must fit int64), NULL arrays, or a label outside [0, n) (counts are then
+ * meaningless).  Workspace: twc_partition_stats_workspace_bytes(n, m, rb) (device, 256-byte
+ * aligned; may be NULL when n = 0).
+ * ------------------------------------------------------------------------------------- */
+size_t twc_partition_stats_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes);
+twc_status twc_partition_stats(const twc_csr *g, const int32_t *labels, int32_t k,
+                               void *workspace, size_t workspace_bytes, int64_t *counts,
+                               double *modularity, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * twc_select_threshold -- the paper's two rules of thumb for picking delta (
+ * reading C22), on HOST arrays describing k sweep points (any order):
+ *   deltas[k], largest[k] (size of the largest community at deltas[i], counts[4i + 1] of
+ *   twc_partition_stats), modularity[k], n = number of vertices (normalises largest).
+ * Rule 1 (TWC_RULE_LARGEST_JUMP): scanning the points by DECREASING delta, find the step with
+ * the largest increase (double)(largest_next - largest_prev) / (double)n (first such step on
+ * ties); if it is >= jump_factor (0.1 is the documented default, not a paper value), select
+ * the higher delta of that step ("a sudden increment in the size of the largest community").
+ * Rule 2 (TWC_RULE_MAX_MODULARITY), otherwise: the delta with the largest modularity, the
+ * larger delta on ties; NaN never wins.  Equal deltas keep input order.
+ * Writes *index (into deltas) and *rule.  TWC_EINVAL: k < 1, n < 1, NULL, NaN delta.
+ * Host-only; no device work.
+ * ------------------------------------------------------------------------------------- */
+typedef enum { TWC_RULE_LARGEST_JUMP = 0, TWC_RULE_MAX_MODULARITY = 1 } twc_rule;
+twc_status twc_select_threshold(const double *deltas, const int64_t *largest,
+                                const double *modularity, int32_t k, int64_t n,
+                                double jump_factor, int32_t *index, int32_t *rule);
+
+/* ---------------------------------------------------------------------------------------
  * twc_validate_csr -- checks the a0 precondition: rowptr[0] = 0, rowptr
  * non-decreasing, rowptr[n] = 2m, 0 <= colidx < n, rows strictly increasing, no self-loops,
  * symmetry.  Writes a bit mask to *verdict (device int32; 0 = valid; bit 0 rowptr, bit 1 id

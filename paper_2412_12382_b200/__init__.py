@@ -11,6 +11,9 @@ There is no CPU fallback: if libtwc.so is missing or no CUDA device is present, 
     out               = twc_pipeline_host(rowptr_h, colidx_h, deltas)   # host in, host out
     t, wedge, tw, labels, stats = twc_score_sweep(rowptr, colidx, deltas)   # fused device path
     twc_validate_csr(rowptr, colidx)                                # raises TwcError if invalid
+    counts, q         = twc_partition_stats(rowptr, colidx, labels)  # int64[k, 4], float64[k]
+    index, rule       = twc_select_threshold(deltas, largest, q, n)  # host, rules of thumb
+    report            = sweep_report(rowptr, colidx, deltas)         # the selection workflow
 
 rowptr: int32 or int64 tensor [n+1]; colidx: int32 tensor [2m] (CUDA tensors, except for
 twc_pipeline_host which takes CPU tensors, ideally pinned).  Outputs are in canonical edge
@@ -75,6 +78,9 @@ def load_library(path: str = LIB_PATH):
         "twc_score_sweep": (ctypes.c_int, [CP, P, I32, P, SZ, P, P, P, P, P, P, P]),
         "twc_similarity": (ctypes.c_int, [CP, P, I32, P, SZ, P, P]),
         "twc_sweep_f64": (ctypes.c_int, [CP, P, P, I32, P, SZ, P, P, P]),
+        "twc_partition_stats_workspace_bytes": (SZ, [I64, I64, I32]),
+        "twc_partition_stats": (ctypes.c_int, [CP, P, I32, P, SZ, P, P, P]),
+        "twc_select_threshold": (ctypes.c_int, [P, P, P, I32, I64, ctypes.c_double, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -309,3 +315,72 @@ def twc_validate_csr(rowptr, colidx, stream=None):
     verdict = torch.zeros(1, dtype=torch.int32, device=colidx.device)
     _check(lib.twc_validate_csr(ctypes.byref(g), _ptr(verdict), _stream(stream)))
     return 0
+
+
+RULES = {0: "largest_cc_jump", 1: "max_modularity"}
+
+
+def twc_partition_stats(rowptr, colidx, labels, counts=None, modularity=None, workspace=None,
+                        stream=None):
+    """Per-partition statistics of labels [k, n] (or [n]) on the input
+    graph: counts [k, 4] = (n_communities, largest, intra_edges, sum_deg_sq) and the
+    modularity [k] (float64).  Synchronises the stream."""
+    lib = load_library()
+    g, n, m = _graph(rowptr, colidx)
+    dev = colidx.device
+    lab = labels.reshape(-1, n) if n > 0 else labels.reshape(-1, 0)
+    if labels.dtype != torch.int32 or not labels.is_contiguous() or not labels.is_cuda:
+        raise ValueError("labels must be a contiguous int32 CUDA tensor")
+    k = lab.shape[0] if n > 0 else max(1, labels.numel())
+    if counts is None:
+        counts = torch.empty((k, 4), dtype=torch.int64, device=dev)
+    if modularity is None:
+        modularity = torch.empty(k, dtype=torch.float64, device=dev)
+    ws = _workspace(lib.twc_partition_stats_workspace_bytes(n, m, rowptr.element_size()), dev,
+                    workspace)
+    _check(lib.twc_partition_stats(ctypes.byref(g), _ptr(labels), k, _ptr(ws), ws.numel(),
+                                   _ptr(counts), _ptr(modularity), _stream(stream)))
+    return counts, modularity
+
+
+def twc_select_threshold(deltas, largest, modularity, n, jump_factor=0.1):
+    """The rules of thumb of P:895-900 (reading C22) over k sweep points (host values):
+    returns (index into deltas, rule name)."""
+    lib = load_library()
+    k = len(deltas)
+    d = (ctypes.c_double * k)(*[float(x) for x in deltas])
+    lg = (ctypes.c_int64 * k)(*[int(x) for x in largest])
+    q = (ctypes.c_double * k)(*[float(x) for x in modularity])
+    idx, rule = ctypes.c_int32(-1), ctypes.c_int32(-1)
+    _check(lib.twc_select_threshold(ctypes.cast(d, ctypes.c_void_p), ctypes.cast(lg, ctypes.c_void_p),
+                                    ctypes.cast(q, ctypes.c_void_p), k, int(n), float(jump_factor),
+                                    ctypes.byref(idx), ctypes.byref(rule)))
+    return int(idx.value), RULES[rule.value]
+
+
+def sweep_report(rowptr, colidx, deltas, tw=None, jump_factor=0.1, stream=None):
+    """The threshold-selection workflow: score once (unless tw is
+    given), filter + label at every delta, the statistics of each partition and the selected
+    delta.  Returns {"points": [{delta, norm_cc, norm_edges, norm_largest_cc, modularity,
+    n_cc, kept, largest, intra_edges, sum_deg_sq}, ...] in input order, "selected_delta",
+    "selected_index", "rule", "labels" (device [k, n])}."""
+    n = rowptr.numel() - 1
+    m = colidx.numel() // 2
+    if tw is None:
+        _, _, tw, labels, stats = twc_score_sweep(rowptr, colidx, deltas, stream=stream)
+    else:
+        labels, stats = twc_sweep(rowptr, colidx, tw, deltas, stream=stream)
+    counts, q = twc_partition_stats(rowptr, colidx, labels, stream=stream)
+    counts, q, stats = counts.cpu().tolist(), q.cpu().tolist(), stats.cpu().tolist()
+    pts = []
+    for d, c, qq, st in zip(deltas, counts, q, stats):
+        pts.append({"delta": float(d), "n_cc": c[0], "largest": c[1], "intra_edges": c[2],
+                    "sum_deg_sq": c[3], "kept": st[0], "modularity": qq,
+                    "norm_cc": c[0] / n if n else float("nan"),
+                    "norm_edges": st[0] / m if m else float("nan"),
+                    "norm_largest_cc": c[1] / n if n else float("nan")})
+    out = {"points": pts, "labels": labels}
+    if n > 0:
+        i, rule = twc_select_threshold(deltas, [p["largest"] for p in pts], q, n, jump_factor)
+        out.update(selected_index=i, selected_delta=float(deltas[i]), rule=rule)
+    return out

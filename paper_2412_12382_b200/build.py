@@ -10,7 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtwc.so")
-SOURCES = ["twc_scan.cu", "twc_score.cu", "twc_cluster.cu", "twc_similarity.cu", "twc_api.cu"]
+SOURCES = ["twc_scan.cu", "twc_score.cu", "twc_cluster.cu", "twc_similarity.cu", "twc_stats.cu",
+           "twc_api.cu"]
 HEADERS = ["twc_common.cuh", "twc_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

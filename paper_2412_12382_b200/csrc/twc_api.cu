@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <string>
+#include <vector>
 
 #include "twc.h"
 #include "twc_internal.h"
@@ -384,6 +385,83 @@ twc_status twc_validate_csr(const twc_csr* g, int32_t* verdict, void* stream) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_status(e, "twc_validate_csr");
     if (h) return fail(TWC_EGRAPH, "CSR invalid, verdict bits 0x%x", h);
+    return TWC_OK;
+}
+
+// ---- threshold selection (NEXT(2)) -------------------------------------------------------
+size_t twc_partition_stats_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes) {
+    (void)rowptr_bytes;
+    if (n < 0 || m < 0) return 0;
+    return partition_stats_ws_bytes(n, m);
+}
+
+twc_status twc_partition_stats(const twc_csr* g, const int32_t* labels, int32_t k, void* ws,
+                               size_t ws_bytes, int64_t* counts, double* modularity,
+                               void* stream) {
+    g_err.clear();
+    twc_status st = check_csr(g);
+    if (st) return st;
+    if (k < 1 || k > 1024) return fail(TWC_EINVAL, "k=%d must be in [1, 1024]", k);
+    if (g->m > 1500000000LL) return fail(TWC_EINVAL, "m=%lld: 4m^2 must fit int64", (long long)g->m);
+    if (g->n > 0 && !labels) return fail(TWC_EINVAL, "labels is NULL");
+    if (!counts) return fail(TWC_EINVAL, "counts is NULL");
+    if (g->n > 0) {
+        st = check_ws(ws, ws_bytes, partition_stats_ws_bytes(g->n, g->m));
+        if (st) return st;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int bad = 0;
+    cudaError_t e;
+    if (g->rowptr_bytes == 4)
+        e = partition_stats_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx,
+                                      labels, k, ws, ws_bytes, reinterpret_cast<long long*>(counts),
+                                      modularity, &bad, s);
+    else
+        e = partition_stats_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr),
+                                            g->colidx, labels, k, ws, ws_bytes,
+                                            reinterpret_cast<long long*>(counts), modularity, &bad, s);
+    if (e != cudaSuccess) return cuda_status(e, "twc_partition_stats");
+    if (bad) return fail(TWC_EINVAL, "a label lies outside [0, n)");
+    return TWC_OK;
+}
+
+twc_status twc_select_threshold(const double* deltas, const int64_t* largest,
+                                const double* modularity, int32_t k, int64_t n,
+                                double jump_factor, int32_t* index, int32_t* rule) {
+    g_err.clear();
+    if (k < 1) return fail(TWC_EINVAL, "k=%d must be >= 1", k);
+    if (!deltas || !largest || !modularity || !index || !rule)
+        return fail(TWC_EINVAL, "NULL argument");
+    if (n < 1) return fail(TWC_EINVAL, "n=%lld must be >= 1", (long long)n);
+    for (int i = 0; i < k; ++i)
+        if (isnan(deltas[i])) return fail(TWC_EINVAL, "delta is NaN");
+    std::vector<int> by(k);
+    for (int i = 0; i < k; ++i) by[i] = i;
+    // decreasing delta; equal deltas keep their input order
+    std::stable_sort(by.begin(), by.end(), [&](int a, int b) { return deltas[a] > deltas[b]; });
+    // rule of thumb 1: the largest increase of the largest community on that scan
+    int jump_at = -1;
+    double jump = 0.0;
+    for (int i = 1; i < k; ++i) {
+        const double inc = (double)(largest[by[i]] - largest[by[i - 1]]) / (double)n;
+        if (jump_at < 0 || inc > jump) {
+            jump = inc;
+            jump_at = by[i - 1];
+        }
+    }
+    if (jump_at >= 0 && jump >= jump_factor) {
+        *index = jump_at;
+        *rule = TWC_RULE_LARGEST_JUMP;
+        return TWC_OK;
+    }
+    // rule of thumb 2: maximum modularity, the larger delta on ties, NaN never wins
+    int best = by[0];
+    for (int i = 1; i < k; ++i) {
+        const double a = modularity[by[i]], b = modularity[best];
+        if (!isnan(a) && (isnan(b) || a > b)) best = by[i];
+    }
+    *index = best;
+    *rule = TWC_RULE_MAX_MODULARITY;
     return TWC_OK;
 }
 

@@ -108,6 +108,15 @@ cudaError_t sweep_f64_impl(int64_t n, int64_t m, const RP* rowptr, const int* co
                            const double* score, const double* deltas, int k, void* ws,
                            size_t ws_bytes, int* labels, long long* stats, cudaStream_t s);
 
+// ---- partition statistics (twc_stats.cu) ---------------------------------------------------
+size_t partition_stats_ws_bytes(int64_t n, int64_t m);
+// counts: device int64[4k]; q: device double[k] or NULL; *bad_host = 1 if a label is outside
+// [0, n).  Synchronises the stream.
+template <typename RP>
+cudaError_t partition_stats_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+                                 const int* labels, int k, void* ws, size_t ws_bytes,
+                                 long long* counts, double* q, int* bad_host, cudaStream_t s);
+
 // ---- validation (twc_cluster.cu) -----------------------------------------------------------
 template <typename RP>
 cudaError_t validate_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,

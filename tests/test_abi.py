@@ -69,6 +69,39 @@ def test_argument_errors_before_device(lib):
     assert lib.twc_sweep(ctypes.byref(g), P(1), None, 1, None, 0, P(1), None, None) == twc.TWC_EINVAL
     assert lib.twc_validate_csr(ctypes.byref(g), None, None) == twc.TWC_EINVAL
     assert lib.twc_score(None, None, 0, P(1), P(1), P(1), None) == twc.TWC_EINVAL
+    # partition statistics (NEXT(2))
+    assert lib.twc_partition_stats(ctypes.byref(g), P(1), 0, None, 0, P(1), None, None) == twc.TWC_EINVAL
+    assert lib.twc_partition_stats(ctypes.byref(g), None, 1, None, 0, P(1), None, None) == twc.TWC_EINVAL
+    assert lib.twc_partition_stats(ctypes.byref(g), P(1), 1, None, 0, None, None, None) == twc.TWC_EINVAL
+    assert lib.twc_partition_stats(ctypes.byref(g), P(1), 1, None, 0, P(1), None, None) == twc.TWC_EWORKSPACE
+    big = _csr(1 << 30, 1_600_000_000, rb=8)
+    assert lib.twc_partition_stats(ctypes.byref(big), P(1), 1, None, 0, P(1), None, None) == twc.TWC_EINVAL
+    assert b"4m^2" in lib.twc_last_error()
+    assert lib.twc_partition_stats_workspace_bytes(4_000_000, 35_000_000, 8) >= 12 * 4_000_000
+
+
+def _select(lib, deltas, largest, q, n, jump=0.1):
+    k = len(deltas)
+    d = (ctypes.c_double * k)(*deltas)
+    lg = (ctypes.c_int64 * k)(*largest)
+    qq = (ctypes.c_double * k)(*q)
+    i, r = ctypes.c_int32(-1), ctypes.c_int32(-1)
+    st = lib.twc_select_threshold(ctypes.cast(d, ctypes.c_void_p), ctypes.cast(lg, ctypes.c_void_p),
+                                  ctypes.cast(qq, ctypes.c_void_p), k, n, jump, ctypes.byref(i),
+                                  ctypes.byref(r))
+    return st, i.value, r.value
+
+
+def test_select_threshold_is_host_logic(lib):
+    # host-only entry point: runs without a GPU.  S:372: single 0 -> 0.9 jump between 4 and 2.
+    st, i, r = _select(lib, [0, 2, 4, 6, 8], [9, 9, 0, 0, 0], [0.1, 0.2, 0.3, 0.2, 0.1], 10)
+    assert (st, i, r) == (twc.TWC_OK, 2, 0)
+    # constant largest -> max modularity, ties to the larger delta
+    st, i, r = _select(lib, [0, 2, 4, 6], [5, 5, 5, 5], [0.1, 0.4, 0.4, float("nan")], 10)
+    assert (st, i, r) == (twc.TWC_OK, 2, 1)
+    assert _select(lib, [0.0], [1], [0.0], 0)[0] == twc.TWC_EINVAL
+    assert _select(lib, [float("nan"), 1.0], [1, 1], [0.0, 0.0], 5)[0] == twc.TWC_EINVAL
+    assert lib.twc_select_threshold(None, None, None, 0, 1, 0.1, None, None) == twc.TWC_EINVAL
 
 
 def test_empty_graph_score_is_ok_without_device(lib):
