@@ -350,6 +350,28 @@ def main_b200(args):
                 "sweep16_ms": statistics.mean(wev[i][0].elapsed_time(wev[i][2]) for i in range(Ks))}
     separate["step_ms"] = separate["score_ms"] + separate["sweep16_ms"]
 
+    # ---- NEXT(2): statistics of the k partitions + the selection rules (reported, not in value)
+    ws_ps = torch.empty(max(1, twc.twc_partition_stats_workspace_bytes(n, m, rb)),
+                        dtype=torch.uint8, device=dev)
+    counts = torch.empty((k, 4), dtype=torch.int64, device=dev)
+    qv = torch.empty(k, dtype=torch.float64, device=dev)
+    twc.twc_partition_stats(rp, ci, labels, counts=counts, modularity=qv, workspace=ws_ps)
+    st_ms = []
+    for _ in range(3):
+        flush.zero_()
+        e0, e1 = mk(2)
+        e0.record(stream)
+        twc.twc_partition_stats(rp, ci, labels, counts=counts, modularity=qv, workspace=ws_ps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        st_ms.append(e0.elapsed_time(e1))
+    cl, ql, sl = counts.cpu().tolist(), qv.cpu().tolist(), stats.cpu().tolist()
+    idx, rule = twc.twc_select_threshold(deltas, [c[1] for c in cl], ql, n)
+    selection = {"partition_stats_ms": statistics.mean(st_ms), "k": k,
+                 "selected_delta": deltas[idx], "rule": rule, "modularity": ql[idx],
+                 "norm_cc": cl[idx][0] / n, "norm_edges": sl[idx][0] / m,
+                 "norm_largest_cc": cl[idx][1] / n}
+
     # ---- roofline of the dominant kernel (K2, oriented intersection), DESIGN.md Sec. 5
     S, dplus_max = orientation_stats(g)
     T = int(t.sum(dtype=torch.int64).item()) // 3
@@ -401,7 +423,7 @@ def main_b200(args):
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": "explicit 512 MiB L2 flush between timed steps; inputs (CSR 312 MB) "
                              "and outputs exceed the 126 MB L2"},
-            "phases_ms": phases, "separate_calls_ms": separate,
+            "phases_ms": phases, "separate_calls_ms": separate, "selection": selection,
             "score_edges_per_s": world * m / (phases["score"] / 1000.0),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": csum, "wall_s_timed": wall,

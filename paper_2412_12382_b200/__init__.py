@@ -320,6 +320,10 @@ def twc_validate_csr(rowptr, colidx, stream=None):
 RULES = {0: "largest_cc_jump", 1: "max_modularity"}
 
 
+def twc_partition_stats_workspace_bytes(n, m, rowptr_bytes=4):
+    return int(load_library().twc_partition_stats_workspace_bytes(n, m, rowptr_bytes))
+
+
 def twc_partition_stats(rowptr, colidx, labels, counts=None, modularity=None, workspace=None,
                         stream=None):
     """Per-partition statistics of labels [k, n] (or [n]) on the input

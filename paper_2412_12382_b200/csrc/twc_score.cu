@@ -242,24 +242,37 @@ __global__ void __launch_bounds__(kSlotThreads) k1_write(
     }
 }
 
-// K1r: rp_or[u] = #out(q < rowptr[u]), eoff[u] = #upper(q < rowptr[u]); rp_or[n] = eoff[n] = m.
+// K1r: rp_or[u] = #out(q < rowptr[u]), eoff[u] = #upper(q < rowptr[u]); rp_or[n] = eoff[n] = m;
+// vinfo[u] = {deg(u), rp_or[u], rp_or[u+1], 0}: everything K3 needs about the far endpoint of
+// an edge in one 16-byte record (one sector per random lookup instead of two).
+template <typename RP>
+__device__ __forceinline__ int out_before(int64_t m, RP p, const unsigned* __restrict__ obits,
+                                          const int* __restrict__ opre) {
+    if ((int64_t)p >= 2 * m) return (int)m;
+    const int64_t wi = (int64_t)(p >> 5);
+    return opre[wi] + __popc(obits[wi] & ((1u << (p & 31)) - 1u));
+}
+
 template <typename RP>
 __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
                         const unsigned* __restrict__ obits, const unsigned* __restrict__ ubits,
                         const int* __restrict__ opre, const int* __restrict__ upre,
-                        int* __restrict__ rp_or, int* __restrict__ eoff) {
+                        int* __restrict__ rp_or, int* __restrict__ eoff, int4* __restrict__ vinfo) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u > n) return;
     const RP p = rowptr[u];
+    const int ob = out_before(m, p, obits, opre);
+    rp_or[u] = ob;
     if ((int64_t)p >= 2 * m) {
-        rp_or[u] = (int)m;
         eoff[u] = (int)m;
-        return;
+    } else {
+        const int64_t wi = (int64_t)(p >> 5);
+        eoff[u] = upre[wi] + __popc(ubits[wi] & ((1u << (p & 31)) - 1u));
     }
-    const int64_t wi = (int64_t)(p >> 5);
-    const unsigned mask = (1u << (p & 31)) - 1u;
-    rp_or[u] = opre[wi] + __popc(obits[wi] & mask);
-    eoff[u] = upre[wi] + __popc(ubits[wi] & mask);
+    if (u < n) {
+        const RP pe = rowptr[u + 1];
+        vinfo[u] = make_int4((int)(pe - p), ob, out_before(m, pe, obits, opre), 0);
+    }
 }
 
 // ---------------------------------------------------------- K2 oriented intersection
@@ -480,11 +493,10 @@ constexpr int kMaxTileRows = 2048;
 template <typename RP, bool BIN>
 __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
-    const int* __restrict__ deg, const int* __restrict__ eoff, const int* __restrict__ trow,
-    const int* __restrict__ rp_or, const int* __restrict__ col_or,
-    const int* __restrict__ opre, const unsigned* __restrict__ obits,
-    const int* __restrict__ t_or, int* __restrict__ t, int* __restrict__ wedge,
-    int* __restrict__ tw, BinSpec bin) {
+    const int4* __restrict__ vinfo, const int* __restrict__ eoff, const int* __restrict__ trow,
+    const int* __restrict__ col_or, const int* __restrict__ opre,
+    const unsigned* __restrict__ obits, const int* __restrict__ t_or, int* __restrict__ t,
+    int* __restrict__ wedge, int* __restrict__ tw, BinSpec bin) {
     constexpr int kIt = kTile / kK3Threads;
     __shared__ int s_off[kMaxTileRows + 1];
     extern __shared__ __align__(8) unsigned char k3_dyn[];  // BIN: thr[k] (i64), hist[k]
@@ -526,16 +538,16 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
             const int du = (int)(rowptr[u + 1] - rb);
             const RP p = rb + (RP)(du - upu) + (RP)(c - eu);  // upper slot of (u,v)
             const int v = __ldcs(colidx + p);
-            // oriented slot if (u,v) is aligned = #out-slots before p (word prefix + popc)
-            const int64_t wi = (int64_t)(p >> 5);
-            const int c2 = opre[wi] + __popc(obits[wi] & ((1u << (p & 31)) - 1u));
-            const int dv = deg[v];
-            const int ob = rp_or[v], oe = rp_or[v + 1];
+            const int4 vi = vinfo[v];  // {deg(v), rp_or[v], rp_or[v+1]}: one random sector
+            const int dv = vi.x;
             int sl;
             if (key_less(du, u, dv, v)) {
-                sl = c2;
+                // aligned: oriented slot = #out-slots before p (word prefix + popc)
+                const int64_t wi = (int64_t)(p >> 5);
+                sl = opre[wi] + __popc(obits[wi] & ((1u << (p & 31)) - 1u));
             } else {  // reversed edge: u's position in N+(v)
-                const int len = oe - ob;
+                const int ob = vi.y;
+                const int len = vi.z - ob;
                 if (len <= 8) {  // short list: independent loads, count entries below u
                     int below = 0;
 #pragma unroll
@@ -598,6 +610,7 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
 struct ScoreWs {
     int *deg, *eoff, *rp_or, *trow, *ftrow, *tile_out, *tile_up, *opre, *upre;
     unsigned *obits, *ubits;
+    int4* vinfo;
     int *col_or, *t_or, *work;
 };
 
@@ -618,6 +631,7 @@ static ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
     w.upre = cv.take<int>(nw);
     w.col_or = cv.take<int>(m);
     w.t_or = cv.take<int>(m);
+    w.vinfo = cv.take<int4>(n);
     w.work = cv.take<int>(1);
     return w;
 }
@@ -658,7 +672,8 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         k1_write<<<grid, kSlotThreads, 0, s>>>(m2, colidx, w.obits, w.ubits, w.tile_out,
                                                w.tile_up, w.opre, w.upre, w.col_or);
         k1_rows<RP><<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, m, rowptr, w.obits, w.ubits,
-                                                                   w.opre, w.upre, w.rp_or, w.eoff);
+                                                                   w.opre, w.upre, w.rp_or, w.eoff,
+                                                                   w.vinfo);
         count_launches(4);
     }
     tile_first_rows(w.eoff, (int)n, m, w.trow, s);
@@ -685,14 +700,13 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         const int64_t nt = num_tiles(m);
         const int grid = grid_for(nt, 1, sms * 8);
         if (bin)
-            k3_score<RP, true><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(m, rowptr, colidx, w.deg, w.eoff, w.trow,
-                                                           w.rp_or, w.col_or, w.opre, w.obits,
-                                                           w.t_or, t, wedge, tw, *bin);
+            k3_score<RP, true><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
+                m, rowptr, colidx, w.vinfo, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
+                wedge, tw, *bin);
         else
-            k3_score<RP, false><<<grid, kK3Threads, 0, s>>>(m, rowptr, colidx, w.deg, w.eoff,
-                                                            w.trow, w.rp_or, w.col_or, w.opre,
-                                                            w.obits, w.t_or, t, wedge, tw,
-                                                            BinSpec{});
+            k3_score<RP, false><<<grid, kK3Threads, 0, s>>>(
+                m, rowptr, colidx, w.vinfo, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
+                wedge, tw, BinSpec{});
         count_launches(1);
         record(ev, 3, s);
     }

@@ -10,17 +10,19 @@
 // and the modularity of P:350-352 as one IEEE division of exact integers (reading C21):
 //     Q = (4 m E_in - sum_c D_c^2) / (4 m^2).
 //
-// Kernels (all HBM/L2 streaming; none is a contraction):
-//   k_part_vertex  one pass over the labels and degrees: per-label size and D_c by atomics into
-//                  two n-long arrays.  Each lane run-length-encodes its strided labels (a giant
-//                  component costs one atomic per run, not per vertex) and a warp merges the
-//                  runs that end on the same label with __match_any_sync.
-//   k_part_roots   one pass over the label-indexed arrays: count / max / sum of squares of the
-//                  non-empty entries, and resets them to zero for the next partition.
-//   k_part_edges   one pass over the CSR for a GROUP of G partitions whose label arrays fit the
-//                  L2 together (G * 4n bytes <= ~48 MB): per slot (u, v), v > u, compares
-//                  labels[u] and labels[v] of each partition of the group -- the gathers hit L2.
-//   k_modularity   one thread per partition.
+// Kernels (HBM streaming plus one random 32-byte gather per edge; none is a contraction):
+//   k_part_degrees  deg[u] once.
+//   k_part_vertex   per partition: one coalesced pass over its labels; per label one packed
+//                   64-bit counter (size << 32 | D_c; D_c <= 2m < 2^32) updated with one atomic
+//                   per distinct label per warp (__match_any_sync).  A warp keeps a "hot" label
+//                   (the last label held by >= 4 lanes of one warp load) in lane-local registers, so a giant
+//                   component costs no atomics at all (same-address atomics serialise).
+//   k_part_roots    per partition: count / max / sum of squares over the non-zero counters.
+//   k_part_pack     per chunk of 8 partitions: labels [8][n] -> [n][8] (32 bytes per vertex).
+//   k_part_edges    per chunk: one pass over the CSR slots (8 consecutive slots per thread, one
+//                   row search, then a walk); for every slot (u, v) with v > u one 32-byte gather
+//                   of v's 8 labels compared with u's -> E_in of all 8 partitions at once.
+//   k_modularity    one thread per partition.
 #include <algorithm>
 
 #include "twc_common.cuh"
@@ -29,90 +31,90 @@
 namespace twc {
 
 constexpr int kStatThreads = 256;
-constexpr int kVertItems = 8;       // vertices per lane in k_part_vertex
-constexpr int kEdgeRows = 2048;     // rowptr entries cached per edge tile
-constexpr int kMaxGroup = 8;        // partitions per k_part_edges pass
-static_assert(kTile % kStatThreads == 0, "k_part_edges: whole slots per thread");
+constexpr int kChunk = 8;                               // partitions per packed edge pass
+constexpr int kEdgeItems = 8;                           // slots per thread in k_part_edges
+constexpr int kEdgeTile = kStatThreads * kEdgeItems;    // 2048 slots
+constexpr int kEdgeRows = 1024;                         // rowptr entries cached per tile
 
 template <typename RP>
+__global__ void k_part_degrees(int64_t n, const RP* __restrict__ rowptr, int* __restrict__ deg) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n) deg[u] = (int)(rowptr[u + 1] - rowptr[u]);
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    return x;
+}
+
 __global__ void __launch_bounds__(kStatThreads) k_part_vertex(
-    int64_t n, const RP* __restrict__ rowptr, const int* __restrict__ lab,
-    int* __restrict__ size, unsigned long long* __restrict__ dsum, int* __restrict__ bad) {
+    int64_t n, const int* __restrict__ deg, const int* __restrict__ lab,
+    unsigned long long* __restrict__ packed, int* __restrict__ bad) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = warp * 32 * kVertItems; base < n; base += nwarps * 32 * kVertItems) {
-        int cur = -1, cnt = 0;
-        unsigned long long ds = 0;
-#pragma unroll
-        for (int i = 0; i < kVertItems; ++i) {
-            const int64_t u = base + i * 32 + lane;
-            if (u >= n) break;
-            const int l = __ldcs(lab + u);
-            const unsigned long long d = (unsigned long long)(rowptr[u + 1] - rowptr[u]);
+    int hot = -1;                   // warp-uniform
+    unsigned long long hacc = 0;    // lane-local (count << 32 | degree sum) of the hot label
+    for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+        const int64_t u = base + lane;
+        int l = -1;
+        unsigned d = 0;
+        if (u < n) {
+            l = __ldcs(lab + u);
+            d = (unsigned)deg[u];
             if (l < 0 || (int64_t)l >= n) {
                 atomicOr(bad, 1);
-                continue;
+                l = -1;
             }
-            if (l != cur) {
-                if (cnt) {
-                    atomicAdd(size + cur, cnt);
-                    atomicAdd(dsum + cur, ds);
-                }
-                cur = l;
-                cnt = 0;
-                ds = 0;
-            }
-            ++cnt;
-            ds += d;
         }
-        // merge the open runs of the warp that end on the same label (typical: one giant label)
-        const unsigned grp = __match_any_sync(0xffffffffu, cur);
-        const int leader = __ffs(grp) - 1;
-        int csum = __reduce_add_sync(grp, (unsigned)cnt);
-        unsigned long long dtot = 0;
-        for (int src = 0; src < 32; ++src) {
-            const unsigned long long v = __shfl_sync(0xffffffffu, ds, src);
-            if ((grp >> src) & 1u) dtot += v;
-        }
-        if (lane == leader && cur >= 0 && csum) {
-            atomicAdd(size + cur, csum);
-            atomicAdd(dsum + cur, dtot);
+        if (l >= 0 && l == hot) hacc += (1ull << 32) | d;
+        const unsigned grp = __match_any_sync(FULL, l);
+        // degrees of distinct vertices: the group sum is <= 2m < 2^32
+        const unsigned dg = __reduce_add_sync(grp, d);
+        const int gsz = __popc(grp);
+        if (l >= 0 && l != hot && lane == __ffs(grp) - 1)
+            atomicAdd(packed + l, ((unsigned long long)gsz << 32) + dg);
+        const unsigned big = __ballot_sync(FULL, gsz >= 4 && l >= 0 && l != hot);
+        if (big) {  // a new frequent label: flush the old hot one, adopt the new
+            const unsigned long long tot = warp_sum_u64(hacc);
+            if (lane == 0 && hot >= 0 && tot) atomicAdd(packed + hot, tot);
+            hacc = 0;
+            hot = __shfl_sync(FULL, l, __ffs(big) - 1);
         }
     }
+    const unsigned long long tot = warp_sum_u64(hacc);
+    if (lane == 0 && hot >= 0 && tot) atomicAdd(packed + hot, tot);
 }
 
-// acc[4j + 0] communities, [4j + 1] largest, [4j + 3] sum of D_c^2 (as unsigned long long)
+// acc[0] communities, [1] largest, [3] sum of D_c^2 (as unsigned long long)
 __global__ void __launch_bounds__(kStatThreads) k_part_roots(
-    int64_t n, int* __restrict__ size, unsigned long long* __restrict__ dsum,
-    unsigned long long* __restrict__ acc) {
+    int64_t n, const unsigned long long* __restrict__ packed, unsigned long long* __restrict__ acc) {
     __shared__ unsigned long long s_cnt, s_sq;
-    __shared__ int s_max;
+    __shared__ unsigned s_max;
     if (threadIdx.x == 0) {
         s_cnt = 0;
         s_sq = 0;
         s_max = 0;
     }
     __syncthreads();
-    unsigned long long cnt = 0, sq = 0;
-    int mx = 0;
+    unsigned cnt = 0, mx = 0;
+    unsigned long long sq = 0;
     for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n;
          l += (int64_t)gridDim.x * blockDim.x) {
-        const int sz = size[l];
-        if (sz) {
-            const unsigned long long d = dsum[l];
+        const unsigned long long x = __ldcs(packed + l);
+        if (x) {
+            const unsigned long long dc = x & 0xffffffffull;
             ++cnt;
-            sq += d * d;
-            mx = max(mx, sz);
-            size[l] = 0;
-            dsum[l] = 0;
+            sq += dc * dc;
+            mx = max(mx, (unsigned)(x >> 32));
         }
     }
-    cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
-    mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)mx);
-    for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    if ((threadIdx.x & 31) == 0 && (cnt || mx)) {
-        atomicAdd(&s_cnt, cnt);
+    cnt = __reduce_add_sync(FULL, cnt);
+    mx = __reduce_max_sync(FULL, mx);
+    sq = warp_sum_u64(sq);
+    if ((threadIdx.x & 31) == 0 && cnt) {
+        atomicAdd(&s_cnt, (unsigned long long)cnt);
         atomicAdd(&s_sq, sq);
         atomicMax(&s_max, mx);
     }
@@ -124,53 +126,97 @@ __global__ void __launch_bounds__(kStatThreads) k_part_roots(
     }
 }
 
-// E_in for partitions j0 .. j0+G-1: acc[4j + 2]
+// labT[u * 8 + i] = lab[i * n + u] for i < g (unused lanes -1)
+__global__ void k_part_pack(int64_t n, const int* __restrict__ lab, int g, int4* __restrict__ labT) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    int x[kChunk];
+#pragma unroll
+    for (int i = 0; i < kChunk; ++i) x[i] = (i < g) ? __ldcs(lab + (int64_t)i * n + u) : -1;
+    labT[2 * u] = make_int4(x[0], x[1], x[2], x[3]);
+    labT[2 * u + 1] = make_int4(x[4], x[5], x[6], x[7]);
+}
+
+__device__ __forceinline__ void count_equal(const int4& a, const int4& b, const int4& ua,
+                                            const int4& ub, int* c) {
+    c[0] += a.x == ua.x; c[1] += a.y == ua.y; c[2] += a.z == ua.z; c[3] += a.w == ua.w;
+    c[4] += b.x == ub.x; c[5] += b.y == ub.y; c[6] += b.z == ub.z; c[7] += b.w == ub.w;
+}
+
+// E_in of the (up to 8) partitions packed in labT: acc[4i + 2]
 template <typename RP>
 __global__ void __launch_bounds__(kStatThreads) k_part_edges(
-    int64_t n, int64_t slots, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
-    const int* __restrict__ trow, const int* __restrict__ lab, int G,
+    int64_t slots, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
+    const int* __restrict__ trow, const int4* __restrict__ labT, int g,
     unsigned long long* __restrict__ acc) {
-    __shared__ RP s_off[kEdgeRows + 1];
-    __shared__ unsigned long long s_in[kMaxGroup];
-    if (threadIdx.x < kMaxGroup) s_in[threadIdx.x] = 0;
-    const int64_t ntiles = num_tiles(slots);
+    __shared__ RP s_rp[kEdgeRows + 1];
+    __shared__ unsigned long long s_in[kChunk];
+    if (threadIdx.x < kChunk) s_in[threadIdx.x] = 0;
+    const int64_t ntiles = (slots + kEdgeTile - 1) / kEdgeTile;
+    int c[kChunk];
+#pragma unroll
+    for (int i = 0; i < kChunk; ++i) c[i] = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t p0 = tile * kTile;
-        const int64_t p1 = min(p0 + kTile, slots);
+        const int64_t p0 = tile * kEdgeTile;
+        const int64_t p1 = min(p0 + kEdgeTile, slots);
         const int r0 = trow[tile];
         const int nr = trow[tile + 1] - r0 + 1;
         const bool cached = nr <= kEdgeRows;
         __syncthreads();
         if (cached)
-            for (int i = threadIdx.x; i <= nr; i += blockDim.x) s_off[i] = rowptr[r0 + i];
+            for (int i = threadIdx.x; i <= nr; i += blockDim.x) s_rp[i] = rowptr[r0 + i];
         __syncthreads();
-        int c[kMaxGroup];
+        const int64_t q0 = p0 + (int64_t)threadIdx.x * kEdgeItems;
+        if (q0 >= p1) continue;
+        int v[kEdgeItems];
+        if (q0 + kEdgeItems <= p1) {
+            const int4* src = reinterpret_cast<const int4*>(colidx + q0);
+            const int4 a = __ldcs(src), b = __ldcs(src + 1);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        } else {
 #pragma unroll
-        for (int g = 0; g < kMaxGroup; ++g) c[g] = 0;
-        const int64_t p = p0 + threadIdx.x;
-        #pragma unroll
-        for (int it = 0; it < kTile / kStatThreads; ++it) {
-            const int64_t q = p + it * kStatThreads;
-            if (q >= p1) break;
-            const RP qq = (RP)q;
-            const int ri = cached ? last_le(s_off, nr + 1, qq) : last_le(rowptr + r0, nr + 1, qq);
-            const int u = r0 + ri;
-            const int v = __ldcs(colidx + q);
-            if (v > u) {
+            for (int j = 0; j < kEdgeItems; ++j) v[j] = (q0 + j < p1) ? colidx[q0 + j] : -1;
+        }
+        // rows of the 8 slots: one search, then a walk
+        int uj[kEdgeItems];
+        {
+            const RP q = (RP)q0;
+            int ri = cached ? last_le(s_rp, nr + 1, q) : last_le(rowptr + r0, nr + 1, q);
+            RP re = cached ? s_rp[ri + 1] : rowptr[r0 + ri + 1];
 #pragma unroll
-                for (int g = 0; g < kMaxGroup; ++g)
-                    if (g < G) c[g] += (lab[(int64_t)g * n + u] == lab[(int64_t)g * n + v]);
+            for (int j = 0; j < kEdgeItems; ++j) {
+                while ((RP)(q0 + j) >= re && q0 + j < p1) {
+                    ++ri;
+                    re = cached ? s_rp[ri + 1] : rowptr[r0 + ri + 1];
+                }
+                uj[j] = r0 + ri;
             }
         }
+        int ucur = -1;
+        int4 ua = make_int4(0, 0, 0, 0), ub = ua;
 #pragma unroll
-        for (int g = 0; g < kMaxGroup; ++g) {
-            if (g >= G) break;
-            const unsigned w = __reduce_add_sync(0xffffffffu, (unsigned)c[g]);
-            if ((threadIdx.x & 31) == 0 && w) atomicAdd(&s_in[g], (unsigned long long)w);
+        for (int j = 0; j < kEdgeItems; ++j) {
+            if (v[j] > uj[j]) {
+                if (uj[j] != ucur) {
+                    ucur = uj[j];
+                    ua = labT[2 * (int64_t)ucur];
+                    ub = labT[2 * (int64_t)ucur + 1];
+                }
+                const int4 a = labT[2 * (int64_t)v[j]], b = labT[2 * (int64_t)v[j] + 1];
+                count_equal(a, b, ua, ub, c);
+            }
         }
     }
     __syncthreads();
-    if (threadIdx.x < G && s_in[threadIdx.x]) atomicAdd(acc + 4 * threadIdx.x + 2, s_in[threadIdx.x]);
+#pragma unroll
+    for (int i = 0; i < kChunk; ++i) {
+        if (i >= g) break;
+        const unsigned w = __reduce_add_sync(FULL, (unsigned)c[i]);
+        if ((threadIdx.x & 31) == 0 && w) atomicAdd(&s_in[i], (unsigned long long)w);
+    }
+    __syncthreads();
+    if (threadIdx.x < g && s_in[threadIdx.x]) atomicAdd(acc + 4 * threadIdx.x + 2, s_in[threadIdx.x]);
 }
 
 __global__ void k_modularity(int k, long long m, const long long* __restrict__ acc,
@@ -187,10 +233,11 @@ __global__ void k_modularity(int k, long long m, const long long* __restrict__ a
 
 size_t partition_stats_ws_bytes(int64_t n, int64_t m) {
     Carver cv(nullptr, 0);
-    cv.take<int>(n);                       // size
-    cv.take<unsigned long long>(n);        // dsum
-    cv.take<int>(num_tiles(2 * m) + 1);    // tile rows of the full CSR
-    cv.take<int>(1);                       // bad-label flag
+    cv.take<int>(n);                                            // deg
+    cv.take<unsigned long long>(n);                             // packed counters
+    cv.take<int4>(2 * n);                                       // labels of 8 partitions, [n][8]
+    cv.take<int>((2 * m + kEdgeTile - 1) / kEdgeTile + 1);      // tile rows of the full CSR
+    cv.take<int>(1);                                            // bad-label flag
     return cv.used;
 }
 
@@ -204,37 +251,34 @@ cudaError_t partition_stats_impl(int64_t n, int64_t m, const RP* rowptr, const i
     if (e != cudaSuccess) return e;
     if (n > 0) {
         Carver cv(ws, ws_bytes);
-        int* size = cv.take<int>(n);
-        unsigned long long* dsum = cv.take<unsigned long long>(n);
-        int* trow = cv.take<int>(num_tiles(2 * m) + 1);
+        int* deg = cv.take<int>(n);
+        unsigned long long* packed = cv.take<unsigned long long>(n);
+        int4* labT = cv.take<int4>(2 * n);
+        int* trow = cv.take<int>((2 * m + kEdgeTile - 1) / kEdgeTile + 1);
         int* bad = cv.take<int>(1);
-        cudaMemsetAsync(size, 0, sizeof(int) * n, s);
-        cudaMemsetAsync(dsum, 0, sizeof(unsigned long long) * n, s);
         cudaMemsetAsync(bad, 0, sizeof(int), s);
         const int sms = num_sms();
-        const int64_t vwarps = (n + 32 * kVertItems - 1) / (32 * kVertItems);
-        const int vgrid = (int)std::min<int64_t>((vwarps + kStatThreads / 32 - 1) / (kStatThreads / 32),
-                                                 (int64_t)sms * 8);
-        const int rgrid = (int)std::max<int64_t>(
-            1, std::min<int64_t>((n + kStatThreads - 1) / kStatThreads, (int64_t)sms * 8));
+        const unsigned vb = (unsigned)((n + kStatThreads - 1) / kStatThreads);
+        k_part_degrees<RP><<<vb, kStatThreads, 0, s>>>(n, rowptr, deg);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(vb, (int64_t)sms * 8));
         for (int j = 0; j < k; ++j) {
-            k_part_vertex<RP><<<vgrid, kStatThreads, 0, s>>>(n, rowptr, labels + (int64_t)j * n,
-                                                             size, dsum, bad);
-            k_part_roots<<<rgrid, kStatThreads, 0, s>>>(n, size, dsum, acc + 4 * j);
+            cudaMemsetAsync(packed, 0, sizeof(unsigned long long) * n, s);
+            k_part_vertex<<<grid, kStatThreads, 0, s>>>(n, deg, labels + (int64_t)j * n, packed,
+                                                        bad);
+            k_part_roots<<<grid, kStatThreads, 0, s>>>(n, packed, acc + 4 * j);
         }
-        count_launches(2 * k);
+        count_launches(1 + 2 * k);
         if (m > 0) {
             const int64_t slots = 2 * m;
-            tile_rows<RP>(rowptr, (int)n, slots, kTile, trow, s);
-            // partitions per pass: their label arrays should sit in L2 together
-            const int64_t l2_budget = (int64_t)48 << 20;
-            const int G = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxGroup, l2_budget / (4 * n)));
-            const int egrid = (int)std::min<int64_t>(num_tiles(slots), (int64_t)sms * 8);
-            for (int j0 = 0; j0 < k; j0 += G) {
-                const int g = std::min(G, k - j0);
-                k_part_edges<RP><<<egrid, kStatThreads, 0, s>>>(
-                    n, slots, rowptr, colidx, trow, labels + (int64_t)j0 * n, g, acc + 4 * j0);
-                count_launches(1);
+            const int64_t et = (slots + kEdgeTile - 1) / kEdgeTile;
+            tile_rows<RP>(rowptr, (int)n, slots, kEdgeTile, trow, s);
+            const int egrid = (int)std::min<int64_t>(et, (int64_t)sms * 8);
+            for (int j0 = 0; j0 < k; j0 += kChunk) {
+                const int g = std::min(kChunk, k - j0);
+                k_part_pack<<<vb, kStatThreads, 0, s>>>(n, labels + (int64_t)j0 * n, g, labT);
+                k_part_edges<RP><<<egrid, kStatThreads, 0, s>>>(slots, rowptr, colidx, trow, labT,
+                                                                g, acc + 4 * j0);
+                count_launches(2);
             }
         }
         e = cudaMemcpyAsync(bad_host, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
