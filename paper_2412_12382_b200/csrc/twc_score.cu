@@ -487,12 +487,40 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n,
 // found by probing the (short) list N+(v) for u.
 //   wedge = d_u + d_v - 2t - 2   (|N(u) | N(v)| - |N(u) & N(v)| - 2 for a simple graph)
 //   TW    = t - wedge            (Eq. 2)
+// Index of u in the sorted list col_or[ob, oe) (u is present).  The search works on aligned
+// 32-byte sectors (8 ids): it starts at the sector where u would sit if the ids were spread
+// evenly over [0, n) (interpolation) and steps one sector at a time, so a typical lookup
+// touches one or two sectors instead of the log2(len) scattered sectors of a binary search.
+__device__ __forceinline__ int sector_search(const int* __restrict__ col_or, int ob, int oe, int u,
+                                             int64_t n) {
+    const int len = oe - ob;
+    int s = (ob + (int)(((long long)len * u) / n)) & ~7;
+    const int s_lo = ob & ~7, s_hi = (oe - 1) & ~7;
+    s = max(s_lo, min(s, s_hi));
+    for (;;) {
+        const int4* q = reinterpret_cast<const int4*>(col_or + s);
+        const int4 a = __ldg(q), b = __ldg(q + 1);
+        const int x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        const int first = max(ob - s, 0), last = min(oe - s, 8) - 1;  // valid entries [first, last]
+        int fv = 0, lv = 0, below = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            fv = (e == first) ? x[e] : fv;
+            lv = (e == last) ? x[e] : lv;
+            below += (e >= first && e <= last && x[e] < u);
+        }
+        if (s > s_lo && fv > u) { s -= 8; continue; }
+        if (s < s_hi && lv < u) { s += 8; continue; }
+        return s + first + below;
+    }
+}
+
 constexpr int kK3Threads = 256;
 constexpr int kMaxTileRows = 2048;
 
 template <typename RP, bool BIN>
 __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
-    int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
+    int64_t n, int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int4* __restrict__ vinfo, const int* __restrict__ eoff, const int* __restrict__ trow,
     const int* __restrict__ col_or, const int* __restrict__ opre,
     const unsigned* __restrict__ obits, const int* __restrict__ t_or, int* __restrict__ t,
@@ -546,16 +574,7 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
                 const int64_t wi = (int64_t)(p >> 5);
                 sl = opre[wi] + __popc(obits[wi] & ((1u << (p & 31)) - 1u));
             } else {  // reversed edge: u's position in N+(v)
-                const int ob = vi.y;
-                const int len = vi.z - ob;
-                if (len <= 8) {  // short list: independent loads, count entries below u
-                    int below = 0;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) below += (e < len && col_or[ob + e] < u);
-                    sl = ob + below;
-                } else {
-                    sl = ob + lower_bound(col_or + ob, len, u);
-                }
+                sl = sector_search(col_or, vi.y, vi.z, u, n);
             }
             const int tt = t_or[sl];
             const int score = 3 * tt - du - dv + 2;
@@ -701,11 +720,11 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         const int grid = grid_for(nt, 1, sms * 8);
         if (bin)
             k3_score<RP, true><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
-                m, rowptr, colidx, w.vinfo, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
+                n, m, rowptr, colidx, w.vinfo, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
                 wedge, tw, *bin);
         else
             k3_score<RP, false><<<grid, kK3Threads, 0, s>>>(
-                m, rowptr, colidx, w.vinfo, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
+                n, m, rowptr, colidx, w.vinfo, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
                 wedge, tw, BinSpec{});
         count_launches(1);
         record(ev, 3, s);
