@@ -123,11 +123,24 @@ twc_status twc_score_sweep(const twc_csr *g, const double *deltas_host, int32_t 
  * speed; pageable works).  t, wedge, tw: HOST int32[m] each, or NULL to skip that copy-back.
  * labels: HOST int32[k*n] or NULL.  stats: HOST int64[2k] or NULL.  Needs a DEVICE workspace
  * of twc_pipeline_workspace_bytes(n, m, rb, k) (holds the device copies too).
+ * The copies back run on a library-owned second stream as soon as each result is final (the
+ * scores after the epilogue, each threshold's labels after its sweep step), overlapping the
+ * remaining device work; `stream` is made to wait for them.
+ *
+ * twc_pipeline_host_async -- the same without the final synchronisation: all work, including
+ * the copies back, is ordered before anything later enqueued on `stream`.  The host outputs are
+ * valid, and the host inputs, host outputs and workspace may be reused, only once `stream` has
+ * completed.  Two calls on two streams with two workspaces overlap one graph's copies back with
+ * the next graph's copy in and compute (PCIe is full duplex).
  * ------------------------------------------------------------------------------------- */
 size_t twc_pipeline_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes, int32_t k);
 twc_status twc_pipeline_host(const twc_csr *g_host, const double *deltas_host, int32_t k,
                              void *workspace, size_t workspace_bytes, int32_t *t, int32_t *wedge,
                              int32_t *tw, int32_t *labels, int64_t *stats, void *stream);
+twc_status twc_pipeline_host_async(const twc_csr *g_host, const double *deltas_host, int32_t k,
+                                   void *workspace, size_t workspace_bytes, int32_t *t,
+                                   int32_t *wedge, int32_t *tw, int32_t *labels, int64_t *stats,
+                                   void *stream);
 
 /* ---------------------------------------------------------------------------------------
  * twc_similarity -- the other edge similarities of Table 1 from the triangle

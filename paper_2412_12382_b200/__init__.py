@@ -67,6 +67,7 @@ def load_library(path: str = LIB_PATH):
         "twc_sweep": (ctypes.c_int, [CP, P, P, I32, P, SZ, P, P, P]),
         "twc_pipeline_workspace_bytes": (SZ, [I64, I64, I32, I32]),
         "twc_pipeline_host": (ctypes.c_int, [CP, P, I32, P, SZ, P, P, P, P, P, P]),
+        "twc_pipeline_host_async": (ctypes.c_int, [CP, P, I32, P, SZ, P, P, P, P, P, P]),
         "twc_validate_csr": (ctypes.c_int, [CP, P, P]),
         "twc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
         "twc_last_error": (ctypes.c_char_p, []),
@@ -281,11 +282,12 @@ def twc_sweep_f64(rowptr, colidx, score, deltas, labels=None, stats=None, worksp
 
 
 def twc_pipeline_host(rowptr, colidx, deltas, want_scores=True, out=None, workspace=None,
-                      stream=None, device=None):
-    """Host CSR in, host results out: H2D copy, score, sweep, D2H copy, sync (one C call).
+                      stream=None, device=None, asynchronous=False):
+    """Host CSR in, host results out: H2D copy, score, sweep, D2H copy (one C call).
 
     rowptr/colidx: CPU tensors (pinned for full PCIe speed).  Returns dict with host tensors
-    t, wedge, tw (if want_scores), labels [k, n] and stats [k, 2]."""
+    t, wedge, tw (if want_scores), labels [k, n] and stats [k, 2].  asynchronous=True calls
+    twc_pipeline_host_async: the results are valid once `stream` completes."""
     lib = load_library()
     g, n, m = _graph(rowptr, colidx, need_cuda=False)
     deltas = [float(d) for d in deltas]
@@ -301,10 +303,16 @@ def twc_pipeline_host(rowptr, colidx, deltas, want_scores=True, out=None, worksp
     arr = (ctypes.c_double * k)(*deltas)
     ws = _workspace(lib.twc_pipeline_workspace_bytes(n, m, rowptr.element_size(), k), dev,
                     workspace)
-    _check(lib.twc_pipeline_host(ctypes.byref(g), ctypes.cast(arr, ctypes.c_void_p), k,
-                                 _ptr(ws), ws.numel(), _ptr(out.get("t")), _ptr(out.get("wedge")),
-                                 _ptr(out.get("tw")), _ptr(out["labels"]), _ptr(out["stats"]),
-                                 _stream(stream)))
+    fn = lib.twc_pipeline_host_async if asynchronous else lib.twc_pipeline_host
+    _check(fn(ctypes.byref(g), ctypes.cast(arr, ctypes.c_void_p), k, _ptr(ws), ws.numel(),
+              _ptr(out.get("t")), _ptr(out.get("wedge")), _ptr(out.get("tw")),
+              _ptr(out["labels"]), _ptr(out["stats"]), _stream(stream)))
+    if asynchronous:
+        # the device keeps using the workspace and the host buffers after this returns: tie the
+        # workspace to the stream for torch's allocator and keep the inputs referenced from out
+        if stream is not None and ws is not workspace:
+            ws.record_stream(stream)
+        out["_inflight"] = (rowptr, colidx, ws)
     return out
 
 

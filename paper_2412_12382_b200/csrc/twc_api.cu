@@ -84,6 +84,38 @@ static twc_status delta_to_thr(double delta, long long* thr) {
     return TWC_OK;
 }
 
+// A per-thread, per-device copy stream plus events for twc_pipeline_host (created on first use
+// and kept for the life of the process).
+struct CopyLane {
+    int dev = -1;
+    cudaStream_t stream = nullptr;
+    std::vector<cudaEvent_t> ev;  // [0] scores final, [1] copies done, [2 + i] sweep step i
+};
+
+static CopyLane* copy_lane(int k) {
+    static thread_local std::vector<CopyLane> lanes;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    CopyLane* L = nullptr;
+    for (auto& x : lanes)
+        if (x.dev == dev) L = &x;
+    if (!L) {
+        lanes.emplace_back();
+        L = &lanes.back();
+        L->dev = dev;
+        if (cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            lanes.pop_back();
+            return nullptr;
+        }
+    }
+    while ((int)L->ev.size() < k + 2) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        L->ev.push_back(e);
+    }
+    return L;
+}
+
 }  // namespace twc
 
 using namespace twc;
@@ -321,6 +353,16 @@ size_t twc_pipeline_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes, 
 twc_status twc_pipeline_host(const twc_csr* gh, const double* deltas_host, int32_t k, void* ws,
                              size_t ws_bytes, int32_t* t, int32_t* wedge, int32_t* tw,
                              int32_t* labels, int64_t* stats, void* stream) {
+    twc_status st = twc_pipeline_host_async(gh, deltas_host, k, ws, ws_bytes, t, wedge, tw,
+                                            labels, stats, stream);
+    if (st) return st;
+    return cuda_status(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)),
+                       "twc_pipeline_host sync");
+}
+
+twc_status twc_pipeline_host_async(const twc_csr* gh, const double* deltas_host, int32_t k,
+                                   void* ws, size_t ws_bytes, int32_t* t, int32_t* wedge,
+                                   int32_t* tw, int32_t* labels, int64_t* stats, void* stream) {
     g_err.clear();
     twc_status st = check_csr(gh);
     if (st) return st;
@@ -338,33 +380,47 @@ twc_status twc_pipeline_host(const twc_csr* gh, const double* deltas_host, int32
     Carver cv(ws, ws_bytes);
     PipeWs w = carve_pipe(cv, n, m, rb, k);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CopyLane* cl = copy_lane(k);
+    if (!cl) return cuda_status(cudaGetLastError(), "twc_pipeline_host copy stream");
     cudaError_t e = cudaSuccess;
     if (n > 0) e = cudaMemcpyAsync(w.rowptr, gh->rowptr, (size_t)(n + 1) * rb, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && m > 0)
         e = cudaMemcpyAsync(w.colidx, gh->colidx, sizeof(int) * 2 * (size_t)m, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return cuda_status(e, "twc_pipeline_host H2D");
-    twc_csr gd = *gh;
-    gd.rowptr = w.rowptr;
-    gd.colidx = w.colidx;
+    // Results go back on a second stream as soon as they are final, overlapping the copies
+    // with the remaining device work: the scores once the epilogue is done (event [3]), the
+    // labels of each threshold once its sweep step is done.
+    cudaEvent_t ev6[6] = {nullptr, nullptr, nullptr, cl->ev[0], nullptr, nullptr};
+    cudaEvent_t* step_ev = cl->ev.data() + 2;
     if (rb == 4)
-        e = score_sweep_impl<int>(n, m, static_cast<const int*>(gd.rowptr), gd.colidx, thr, k,
+        e = score_sweep_impl<int>(n, m, static_cast<const int*>(w.rowptr), w.colidx, thr, k,
                                   w.inner, w.inner_bytes, w.t, w.wedge, w.tw, w.labels, w.stats,
-                                  s, nullptr);
+                                  s, ev6, step_ev);
     else
-        e = score_sweep_impl<long long>(n, m, static_cast<const long long*>(gd.rowptr), gd.colidx,
+        e = score_sweep_impl<long long>(n, m, static_cast<const long long*>(w.rowptr), w.colidx,
                                         thr, k, w.inner, w.inner_bytes, w.t, w.wedge, w.tw,
-                                        w.labels, w.stats, s, nullptr);
+                                        w.labels, w.stats, s, ev6, step_ev);
     if (e != cudaSuccess) return cuda_status(e, "twc_pipeline_host score_sweep");
+    if (m == 0 || n == 0) cudaEventRecord(cl->ev[0], s);
+    cudaStream_t c = cl->stream;
     const size_t mb = sizeof(int) * (size_t)m;
-    if (t && m) e = cudaMemcpyAsync(t, w.t, mb, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && wedge && m) e = cudaMemcpyAsync(wedge, w.wedge, mb, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && tw && m) e = cudaMemcpyAsync(tw, w.tw, mb, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && labels && n)
-        e = cudaMemcpyAsync(labels, w.labels, sizeof(int) * (size_t)k * n, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamWaitEvent(c, cl->ev[0], 0);
+    if (e == cudaSuccess && t && m) e = cudaMemcpyAsync(t, w.t, mb, cudaMemcpyDeviceToHost, c);
+    if (e == cudaSuccess && wedge && m) e = cudaMemcpyAsync(wedge, w.wedge, mb, cudaMemcpyDeviceToHost, c);
+    if (e == cudaSuccess && tw && m) e = cudaMemcpyAsync(tw, w.tw, mb, cudaMemcpyDeviceToHost, c);
+    SweepPlan P;
+    sweep_plan(thr, k, &P);
+    for (int i = 0; i < k && e == cudaSuccess; ++i) {
+        e = cudaStreamWaitEvent(c, step_ev[i], 0);
+        if (e == cudaSuccess && labels && n)
+            e = cudaMemcpyAsync(labels + (size_t)P.order[i] * n, w.labels + (size_t)P.order[i] * n,
+                                sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost, c);
+    }
     if (e == cudaSuccess && stats)
-        e = cudaMemcpyAsync(stats, w.stats, sizeof(long long) * 2 * (size_t)k, cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) return cuda_status(e, "twc_pipeline_host D2H");
-    return cuda_status(cudaStreamSynchronize(s), "twc_pipeline_host sync");
+        e = cudaMemcpyAsync(stats, w.stats, sizeof(long long) * 2 * (size_t)k, cudaMemcpyDeviceToHost, c);
+    if (e == cudaSuccess) e = cudaEventRecord(cl->ev[1], c);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, cl->ev[1], 0);  // the caller's stream sees all
+    return cuda_status(e, "twc_pipeline_host D2H");
 }
 
 twc_status twc_validate_csr(const twc_csr* g, int32_t* verdict, void* stream) {

@@ -366,7 +366,8 @@ void init_parent(int64_t n, int* parent, cudaStream_t s) {
 
 // Steps in descending threshold order: hook band i, snapshot labels for threshold order[i].
 void sweep_loop(int64_t n, int64_t m, const SweepPlan& P, const int2* pairs, const int* off,
-                int* parent, int* labels, unsigned long long* st, cudaStream_t s) {
+                int* parent, int* labels, unsigned long long* st, cudaStream_t s,
+                cudaEvent_t* step_ev) {
     const int sms = num_sms();
     const int hook_grid = sms * 8;
     const int fin_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
@@ -378,6 +379,7 @@ void sweep_loop(int64_t n, int64_t m, const SweepPlan& P, const int2* pairs, con
         }
         k_finalize<<<fin_grid, 256, 0, s>>>(n, parent, labels + (size_t)idx * n, st + 2 * idx + 1);
         count_launches(1);
+        if (step_ev) cudaEventRecord(step_ev[i], s);  // labels of threshold order[i] final
     }
 }
 
@@ -463,14 +465,17 @@ template <typename RP>
 cudaError_t score_sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
                              const long long* thr, int k, void* ws, size_t ws_bytes, int* t,
                              int* wedge, int* tw, int* labels, long long* stats, cudaStream_t s,
-                             cudaEvent_t* ev) {
+                             cudaEvent_t* ev, cudaEvent_t* step_ev) {
     Carver cv(ws, ws_bytes);
     FusedWs w = carve_fused(cv, n, m);
     unsigned long long* st = stats ? reinterpret_cast<unsigned long long*>(stats) : w.stats;
     if (m == 0 || n == 0) {  // nothing to score: every vertex is its own component
         for (int i = 0; i < 6; ++i) record(ev, i, s);
-        return sweep_impl<RP>(n, m, rowptr, colidx, tw, thr, k, w.score, w.score_bytes, labels,
-                              stats, s, nullptr);
+        cudaError_t e = sweep_impl<RP>(n, m, rowptr, colidx, tw, thr, k, w.score, w.score_bytes,
+                                       labels, stats, s, nullptr);
+        if (step_ev)
+            for (int i = 0; i < k; ++i) cudaEventRecord(step_ev[i], s);
+        return e;
     }
     SweepPlan P;
     sweep_plan(thr, k, &P);
@@ -486,18 +491,19 @@ cudaError_t score_sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* 
     band_place(w.kept, w.kband, w.nkept, m, k, w.cursor, w.pairs, s);
     init_parent(n, w.parent, s);
     record(ev, 4, s);
-    sweep_loop(n, m, P, w.pairs, w.off, w.parent, labels, st, s);
+    sweep_loop(n, m, P, w.pairs, w.off, w.parent, labels, st, s, step_ev);
     record(ev, 5, s);
     return cudaGetLastError();
 }
 
 template cudaError_t score_sweep_impl<int>(int64_t, int64_t, const int*, const int*,
                                            const long long*, int, void*, size_t, int*, int*,
-                                           int*, int*, long long*, cudaStream_t, cudaEvent_t*);
+                                           int*, int*, long long*, cudaStream_t, cudaEvent_t*,
+                                           cudaEvent_t*);
 template cudaError_t score_sweep_impl<long long>(int64_t, int64_t, const long long*, const int*,
                                                  const long long*, int, void*, size_t, int*,
                                                  int*, int*, int*, long long*, cudaStream_t,
-                                                 cudaEvent_t*);
+                                                 cudaEvent_t*, cudaEvent_t*);
 
 template cudaError_t sweep_impl<int>(int64_t, int64_t, const int*, const int*, const int*,
                                      const long long*, int, void*, size_t, int*, long long*,

@@ -64,8 +64,10 @@ void band_offsets(const int* cnt, int k, const int* order_dev, int* off, int* cu
                   unsigned long long* stats, cudaStream_t s);
 void band_place(const int2* kept, const unsigned short* kband, const int* nkept, int64_t cap,
                 int k, int* cursor, int2* pairs, cudaStream_t s);
+// step_ev: NULL or k events, step_ev[i] recorded once the labels of threshold order[i] are final
 void sweep_loop(int64_t n, int64_t m, const SweepPlan& P, const int2* pairs, const int* off,
-                int* parent, int* labels, unsigned long long* stats, cudaStream_t s);
+                int* parent, int* labels, unsigned long long* stats, cudaStream_t s,
+                cudaEvent_t* step_ev = nullptr);
 void init_parent(int64_t n, int* parent, cudaStream_t s);
 
 // ---- score (twc_score.cu) ------------------------------------------------------------------
@@ -91,7 +93,7 @@ template <typename RP>
 cudaError_t score_sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
                              const long long* thr, int k, void* ws, size_t ws_bytes, int* t,
                              int* wedge, int* tw, int* labels, long long* stats, cudaStream_t s,
-                             cudaEvent_t* ev);
+                             cudaEvent_t* ev, cudaEvent_t* step_ev = nullptr);
 // thresholds already converted to integer "keep iff tw >= thr[i]" form, any order.
 template <typename RP>
 cudaError_t sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, const int* tw,

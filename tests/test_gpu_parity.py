@@ -190,6 +190,29 @@ def test_pipeline_host_matches_device_path(oracle_mod):
         assert out["stats"][i].tolist() == [kept, ncomp]
 
 
+def test_pipeline_host_async_in_flight(oracle_mod):
+    # three graphs in flight on three streams (different sizes, int32 and int64 rowptr, one
+    # with duplicate and unsorted thresholds): every call's host outputs equal the oracle's
+    graphs = [gg.config_graph(1), gg.erdos_renyi(3000, 0.01, seed=4),
+              gg.planted_partition(30, 40, 0.3, 0.01, seed=5).with_rowptr_dtype(np.int64)]
+    deltas = [[-1.0, 0.0, 2.0], [0.0, -3.0, 0.0, -1.0], [-30.0, -10.0, 0.0]]
+    calls = []
+    for g, d in zip(graphs, deltas):
+        st = torch.cuda.Stream()
+        out = twc.twc_pipeline_host(torch.from_numpy(g.rowptr).pin_memory(),
+                                    torch.from_numpy(g.colidx).pin_memory(), d, stream=st,
+                                    asynchronous=True)
+        calls.append((g, d, st, out))
+    for g, d, st, out in calls:
+        st.synchronize()
+        ot, ow, otw = oracle_mod.score(g)
+        assert np.array_equal(out["tw"].numpy(), otw) and np.array_equal(out["t"].numpy(), ot)
+        for i, x in enumerate(d):
+            ol, kept, ncomp = oracle_mod.cluster(g, otw, x)
+            assert np.array_equal(out["labels"][i].numpy(), ol)
+            assert out["stats"][i].tolist() == [kept, ncomp]
+
+
 def test_validate_csr():
     g = gg.config_graph(1)
     rp, ci = harness.to_device(g)
