@@ -83,7 +83,8 @@ template <typename RP>
 __global__ void __launch_bounds__(kSlotThreads, 8) k1_bits(
     int64_t m2, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int* __restrict__ deg, const int* __restrict__ ftrow, unsigned* __restrict__ obits,
-    unsigned* __restrict__ ubits, int* __restrict__ tile_out, int* __restrict__ tile_up) {
+    unsigned* __restrict__ ubits, int* __restrict__ tile_out, int* __restrict__ tile_up,
+    unsigned short* __restrict__ dslot) {
     __shared__ RP s_rp[kMaxSlotRows + 1];
     __shared__ unsigned s_wsum[kSlotThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -106,6 +107,19 @@ __global__ void __launch_bounds__(kSlotThreads, 8) k1_bits(
         int dv[kSlotItems];
 #pragma unroll
         for (int j = 0; j < kSlotItems; ++j) dv[j] = (q0 + j < T.p1) ? deg[v[j]] : 0;
+        // the far endpoint's degree of every slot (saturated at 0xffff), kept for the epilogue:
+        // K3 then needs no random access for an aligned edge
+        if (q0 + kSlotItems <= T.p1) {
+            unsigned w4[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                w4[j] = (unsigned)min(dv[2 * j], 0xffff) | ((unsigned)min(dv[2 * j + 1], 0xffff) << 16);
+            __stcs(reinterpret_cast<uint4*>(dslot + q0), make_uint4(w4[0], w4[1], w4[2], w4[3]));
+        } else {
+#pragma unroll
+            for (int j = 0; j < kSlotItems; ++j)
+                if (q0 + j < T.p1) dslot[q0 + j] = (unsigned short)min(dv[j], 0xffff);
+        }
         unsigned ob = 0, ub = 0;
         if (q0 < T.p1) {
             int ri = slot_row(T, s_rp, rowptr, q0);
@@ -243,8 +257,8 @@ __global__ void __launch_bounds__(kSlotThreads) k1_write(
 }
 
 // K1r: rp_or[u] = #out(q < rowptr[u]), eoff[u] = #upper(q < rowptr[u]); rp_or[n] = eoff[n] = m;
-// vinfo[u] = {deg(u), rp_or[u], rp_or[u+1], 0}: everything K3 needs about the far endpoint of
-// an edge in one 16-byte record (one sector per random lookup instead of two).
+// vinfo[u] = {rp_or[u], rp_or[u+1]}: the oriented list of the far endpoint of a reversed edge
+// in one 8-byte record (one sector per random lookup instead of two).
 template <typename RP>
 __device__ __forceinline__ int out_before(int64_t m, RP p, const unsigned* __restrict__ obits,
                                           const int* __restrict__ opre) {
@@ -257,7 +271,7 @@ template <typename RP>
 __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
                         const unsigned* __restrict__ obits, const unsigned* __restrict__ ubits,
                         const int* __restrict__ opre, const int* __restrict__ upre,
-                        int* __restrict__ rp_or, int* __restrict__ eoff, int4* __restrict__ vinfo) {
+                        int* __restrict__ rp_or, int* __restrict__ eoff, int2* __restrict__ vinfo) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u > n) return;
     const RP p = rowptr[u];
@@ -271,7 +285,7 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
     }
     if (u < n) {
         const RP pe = rowptr[u + 1];
-        vinfo[u] = make_int4((int)(pe - p), ob, out_before(m, pe, obits, opre), 0);
+        vinfo[u] = make_int2(ob, out_before(m, pe, obits, opre));
     }
 }
 
@@ -521,7 +535,9 @@ constexpr int kMaxTileRows = 2048;
 template <typename RP, bool BIN>
 __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     int64_t n, int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
-    const int4* __restrict__ vinfo, const int* __restrict__ eoff, const int* __restrict__ trow,
+    const int2* __restrict__ vinfo, const unsigned short* __restrict__ dslot,
+    const int* __restrict__ deg, const int* __restrict__ eoff,
+    const int* __restrict__ trow,
     const int* __restrict__ col_or, const int* __restrict__ opre,
     const unsigned* __restrict__ obits, const int* __restrict__ t_or, int* __restrict__ t,
     int* __restrict__ wedge, int* __restrict__ tw, BinSpec bin) {
@@ -566,15 +582,18 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
             const int du = (int)(rowptr[u + 1] - rb);
             const RP p = rb + (RP)(du - upu) + (RP)(c - eu);  // upper slot of (u,v)
             const int v = __ldcs(colidx + p);
-            const int4 vi = vinfo[v];  // {deg(v), rp_or[v], rp_or[v+1]}: one random sector
-            const int dv = vi.x;
+            // aligned iff the upper slot p is an out-slot; deg(v) was kept per slot by K1
+            const int64_t wi = (int64_t)(p >> 5);
+            const unsigned ow = obits[wi];
+            int dv = __ldcs(dslot + p);
+            if (dv == 0xffff) dv = deg[v];  // saturated: a vertex of degree >= 65535
             int sl;
-            if (key_less(du, u, dv, v)) {
+            if ((ow >> (p & 31)) & 1u) {
                 // aligned: oriented slot = #out-slots before p (word prefix + popc)
-                const int64_t wi = (int64_t)(p >> 5);
-                sl = opre[wi] + __popc(obits[wi] & ((1u << (p & 31)) - 1u));
-            } else {  // reversed edge: u's position in N+(v)
-                sl = sector_search(col_or, vi.y, vi.z, u, n);
+                sl = opre[wi] + __popc(ow & ((1u << (p & 31)) - 1u));
+            } else {  // reversed edge: u's position in N+(v), one random 8-byte record first
+                const int2 vi = vinfo[v];
+                sl = sector_search(col_or, vi.x, vi.y, u, n);
             }
             const int tt = t_or[sl];
             const int score = 3 * tt - du - dv + 2;
@@ -629,7 +648,8 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
 struct ScoreWs {
     int *deg, *eoff, *rp_or, *trow, *ftrow, *tile_out, *tile_up, *opre, *upre;
     unsigned *obits, *ubits;
-    int4* vinfo;
+    int2* vinfo;
+    unsigned short* dslot;
     int *col_or, *t_or, *work;
 };
 
@@ -650,7 +670,8 @@ static ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
     w.upre = cv.take<int>(nw);
     w.col_or = cv.take<int>(m);
     w.t_or = cv.take<int>(m);
-    w.vinfo = cv.take<int4>(n);
+    w.vinfo = cv.take<int2>(n);
+    w.dslot = cv.take<unsigned short>(2 * m);
     w.work = cv.take<int>(1);
     return w;
 }
@@ -686,7 +707,7 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     {
         const int grid = grid_for(nst, 1, sms * 8);
         k1_bits<RP><<<grid, kSlotThreads, 0, s>>>(m2, rowptr, colidx, w.deg, w.ftrow, w.obits,
-                                                 w.ubits, w.tile_out, w.tile_up);
+                                                 w.ubits, w.tile_out, w.tile_up, w.dslot);
         k1_tile_scan<<<1, 1024, 0, s>>>(nst, w.tile_out, w.tile_up);
         k1_write<<<grid, kSlotThreads, 0, s>>>(m2, colidx, w.obits, w.ubits, w.tile_out,
                                                w.tile_up, w.opre, w.upre, w.col_or);
@@ -720,11 +741,11 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         const int grid = grid_for(nt, 1, sms * 8);
         if (bin)
             k3_score<RP, true><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
-                n, m, rowptr, colidx, w.vinfo, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
+                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
                 wedge, tw, *bin);
         else
             k3_score<RP, false><<<grid, kK3Threads, 0, s>>>(
-                n, m, rowptr, colidx, w.vinfo, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
+                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
                 wedge, tw, BinSpec{});
         count_launches(1);
         record(ev, 3, s);
