@@ -337,22 +337,60 @@ def dc_sbm(n: int, m_target: int, gamma: float, theta_max: float, smin: int, sma
 
 
 def rmat(scale: int, m_req: int, seed: int, a=(0.45, 0.15, 0.15, 0.25),
-         rowptr_dtype=np.int32) -> Graph:
-    """R-MAT with the paper's static seed matrix, no noise; duplicates and self-loops
-    dropped, so the realised m is at most m_req."""
+         rowptr_dtype=np.int32, n: int | None = None, chunk: int = 1 << 24) -> Graph:
+    """R-MAT (Chakrabarti et al.) with the paper's static seed matrix a = (a11, a12, a21, a22)
+    = (0.45, 0.15, 0.15, 0.25), no noise.  Each of the m_req draws descends `scale`
+    levels of the 2x2 recursion (one uniform per level picks the quadrant).  With n given
+    (n <= 2^scale), draws with an endpoint >= n are redrawn, so ids cover exactly [0, n)
+    (reading N3).  Self-loops and duplicate pairs are then dropped, so the realised
+    m is at most m_req.  Draws are generated in chunks to bound memory."""
     rng = np.random.default_rng(seed)
-    n = 1 << scale
-    cp = np.cumsum(np.asarray(a, dtype=np.float64))
-    u = np.zeros(m_req, dtype=np.int64)
-    v = np.zeros(m_req, dtype=np.int64)
-    for lvl in range(scale):
-        r = rng.random(m_req)
-        q = np.searchsorted(cp, r, side="right")
-        q = np.minimum(q, 3)
-        u |= (q >> 1).astype(np.int64) << lvl
-        v |= (q & 1).astype(np.int64) << lvl
-    return csr_from_pairs(n, u, v, rowptr_dtype,
-                          meta={"kind": "rmat", "scale": scale, "m_req": m_req, "seed": seed})
+    nv = (1 << scale) if n is None else int(n)
+    if nv > (1 << scale):
+        raise ValueError("n exceeds 2^scale")
+    c1, c2, c3 = np.cumsum(np.asarray(a, dtype=np.float64))[:3]
+    us, vs, got = [], [], 0
+    while got < m_req:
+        k = min(chunk, m_req - got)
+        u = np.zeros(k, dtype=np.int64)
+        v = np.zeros(k, dtype=np.int64)
+        for lvl in range(scale):
+            r = rng.random(k)
+            q = (r >= c1).astype(np.int64) + (r >= c2) + (r >= c3)  # quadrant 0..3
+            u |= (q >> 1) << lvl
+            v |= (q & 1) << lvl
+        if n is not None:
+            ok = (u < nv) & (v < nv)
+            u, v = u[ok], v[ok]
+        us.append(u)
+        vs.append(v)
+        got += u.size
+    return csr_from_pairs(nv, np.concatenate(us), np.concatenate(vs), rowptr_dtype,
+                          meta={"kind": "rmat", "scale": scale, "n": nv, "m_req": m_req,
+                                "seed": seed, "a": tuple(a)})
+
+
+# R-MAT workloads of Table "tab:syn" (P:728-746; SURVEY 8(f) NEXT(3)): densities very sparse
+# m = 5n, sparse m = 50n, dense m = n^1.5, at 10^7 and 10^8 requested edges.  n is the paper's
+# (rounded as printed; the dense n = m^(2/3)); the R-MAT scale is the smallest with 2^scale >= n.
+RMAT_CONFIGS = {
+    "vs-1e7": dict(n=2_000_000, m=10_000_000, paper_tw_s=1.77),
+    "vs-1e8": dict(n=20_000_000, m=100_000_000, paper_tw_s=20.05),
+    "s-1e7": dict(n=200_000, m=10_000_000, paper_tw_s=4.96),
+    "s-1e8": dict(n=2_000_000, m=100_000_000, paper_tw_s=71.06),
+    "d-1e7": dict(n=46_416, m=10_000_000, paper_tw_s=13.91),
+    "d-1e8": dict(n=215_443, m=100_000_000, paper_tw_s=378.11),
+}
+
+
+def rmat_graph(name: str, seed: int = 11) -> Graph:
+    c = RMAT_CONFIGS[name]
+    n, m = c["n"], c["m"]
+    scale = max(1, int(np.ceil(np.log2(n))))
+    rp = np.int64 if 2 * m >= (1 << 31) else np.int32
+    g = rmat(scale, m, seed, n=n, rowptr_dtype=rp)
+    g.meta["config"] = "rmat-" + name
+    return g
 
 
 # ---------------------------------------------------------------------------------------

@@ -1,0 +1,95 @@
+"""GPU parity on the R-MAT workloads of Table "tab:syn" (a = (0.45, 0.15, 0.15, 0.25),
+P:756).
+
+10^7 requested edges (very sparse m = 5n, sparse m = 50n, dense m = n^1.5): full oracle parity
+of t, wedge, TW (bit-exact) and of the labels at three thresholds (nearest-rank p10 / p50 / p90 of
+TW; R-MAT's TW is negative everywhere, so the paper's SBM grid would keep nothing).
+10^8 requested edges: the oracle scores sampled row windows (every edge of those rows compared
+bit-exact); the labels at full size are checked by properties that hold at any size (min-id
+canonical, every kept edge inside one label, every label connected through kept edges, the
+kept-edge and component counts)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+from scipy.sparse.csgraph import connected_components
+
+import graphgen as gg
+import harness
+import paper_2412_12382_b200 as twc
+from paper_2412_12382_b200 import build as twc_build
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: the gpu tests need a B200 (there is no CPU fallback)")
+    twc_build.build()
+    twc.load_library()
+
+
+def percentile_thresholds(tw):
+    return [harness.nearest_rank(tw, p) for p in (10, 50, 90)]
+
+
+@pytest.mark.parametrize("name", ["vs-1e7", "s-1e7", "d-1e7"])
+def test_rmat_1e7_full_parity(oracle_mod, name):
+    oracle_mod.set_threads(oracle_mod.max_threads())
+    g = gg.rmat_graph(name)
+    ot, ow, otw = oracle_mod.score(g)
+    deltas = percentile_thresholds(otw)
+    rp, ci = harness.to_device(g)
+    t, w, tw, labels, stats = twc.twc_score_sweep(rp, ci, deltas)
+    torch.cuda.synchronize()
+    for a, b, what in ((t, ot, "t"), (w, ow, "wedge"), (tw, otw, "tw")):
+        bad = np.nonzero(a.cpu().numpy() != b)[0]
+        assert bad.size == 0, f"{name} {what}: {bad.size} mismatches, first {bad[:5]}"
+    lab, st = labels.cpu().numpy(), stats.cpu().numpy()
+    for i, d in enumerate(deltas):
+        ol, kept, ncomp = oracle_mod.cluster(g, otw, d)
+        assert np.array_equal(lab[i], ol), (name, d)
+        assert (int(st[i, 0]), int(st[i, 1])) == (kept, ncomp), (name, d)
+
+
+def check_labels_by_properties(g, tw, delta, lab, kept, ncomp):
+    s, d = g.canonical_pairs()
+    keep = ~(tw.astype(np.float64) < delta)
+    assert kept == int(keep.sum())
+    # every kept edge joins one label; labels are min-id canonical and each label is connected
+    assert np.all(lab[s[keep]] == lab[d[keep]])
+    assert np.all(lab <= np.arange(g.n)) and np.all(lab[lab] == lab)
+    A = sp.coo_matrix((np.ones(int(keep.sum())), (s[keep], d[keep])), shape=(g.n, g.n))
+    ncc, cc = connected_components(A, directed=False)
+    assert ncc == ncomp == int(np.sum(lab == np.arange(g.n)))
+    # same partition: the pairs (label, scipy component) are in one-to-one correspondence
+    pairs = np.unique(np.stack([lab, cc]), axis=1)
+    assert pairs.shape[1] == ncc
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["s-1e8"])
+def test_rmat_1e8_sampled_parity(oracle_mod, name):
+    oracle_mod.set_threads(oracle_mod.max_threads())
+    g = gg.rmat_graph(name)
+    rp, ci = harness.to_device(g)
+    t, w, tw = twc.twc_score(rp, ci)
+    torch.cuda.synchronize()
+    t, w, tw = t.cpu().numpy(), w.cpu().numpy(), tw.cpu().numpy()
+    # sampled rows: low ids (the R-MAT hubs), middle and high ids, a ragged end window
+    s_, _ = g.canonical_pairs()
+    eoff = np.searchsorted(s_, np.arange(g.n + 1))  # first canonical id of each row
+    for u0, u1 in [(0, 64), (g.n // 3, g.n // 3 + 500), (g.n // 2, g.n // 2 + 2000),
+                   (g.n - 3000, g.n)]:
+        ot, ow, otw = oracle_mod.score(g, rows=(u0, u1))
+        c0, c1 = int(eoff[u0]), int(eoff[u1])
+        assert np.array_equal(t[c0:c1], ot[c0:c1]), (u0, u1)
+        assert np.array_equal(w[c0:c1], ow[c0:c1]), (u0, u1)
+        assert np.array_equal(tw[c0:c1], otw[c0:c1]), (u0, u1)
+    deltas = percentile_thresholds(tw)
+    twd = torch.from_numpy(tw).cuda()
+    labels, stats = twc.twc_sweep(rp, ci, twd, deltas)
+    lab, st = labels.cpu().numpy(), stats.cpu().numpy()
+    for i, d in enumerate(deltas):
+        check_labels_by_properties(g, tw, d, lab[i], int(st[i, 0]), int(st[i, 1]))
