@@ -389,8 +389,12 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n,
             const int A = rp_or[u];
             const int e_l = (lane < np_max) ? rp_or[u + lane + 1] : INT_MAX;
             const unsigned fit = __ballot_sync(FULL, lane < np_max && e_l - A <= kGroupSlots);
-            const bool staged = fit != 0u;
-            const int np = staged ? __popc(fit) : 1;
+            if (fit == 0u) {  // a hub (|N+(u)| > kGroupSlots): k2_hubs takes it
+                ++u;
+                continue;
+            }
+            const bool staged = true;
+            const int np = __popc(fit);
             const int B = __shfl_sync(FULL, e_l, np - 1);
             if (lane == 0) S.prp[0] = A;
             if (lane < np) S.prp[lane + 1] = e_l;
@@ -490,6 +494,160 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n,
             __syncwarp();
             u += np;
         }
+    }
+}
+
+// ------------------------------------------------------ K2h: hub pivots (|N+(u)| > 256)
+// One pivot per CTA: the whole block stages N+(u) (up to kHubMax entries) and a 64K-bit filter
+// of it in shared memory, and its 8 warps take the pivot's slots 32 at a time with the same
+// flattened-quad scan, filter and candidate ring as K2.  A list longer than kHubMax keeps only
+// the filter; its candidates are verified by binary search in global memory.
+constexpr int kHubMax = 8192;
+constexpr int kHubFilterLog = 16;
+constexpr int kHubFilterWords = (1 << kHubFilterLog) / 32;
+
+struct K2HubWarp {
+    int pre[32], vst[32], vln[32], owner[32];
+    int ring[kRing];
+};
+struct K2HubSmem {
+    int list[kHubMax];
+    int cnt[kHubMax];
+    unsigned filt[kHubFilterWords];
+    K2HubWarp w[kK2Warps];
+    int hub;
+};
+
+__device__ __forceinline__ unsigned hub_hash(int w) {
+    return ((unsigned)w * 2654435761u) >> (32 - kHubFilterLog);
+}
+
+// hubs[] = pivots with more than kGroupSlots oriented neighbours (order irrelevant)
+__global__ void k2_find_hubs(int64_t n, const int* __restrict__ rp_or, int* __restrict__ hubs,
+                             int* __restrict__ nhubs) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool hub = u < n && rp_or[u + 1] - rp_or[u] > kGroupSlots;
+    const unsigned b = __ballot_sync(FULL, hub);
+    if (!b) return;
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == __ffs(b) - 1) base = atomicAdd(nhubs, __popc(b));
+    base = __shfl_sync(FULL, base, __ffs(b) - 1);
+    if (hub) hubs[base + __popc(b & ((1u << lane) - 1u))] = (int)u;
+}
+
+__global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
+    const int* __restrict__ rp_or, const int* __restrict__ col_or, const int* __restrict__ hubs,
+    const int* __restrict__ nhubs, int* __restrict__ work, int* __restrict__ t_or) {
+    extern __shared__ __align__(16) unsigned char k2h_smem_raw[];
+    K2HubSmem& H = *reinterpret_cast<K2HubSmem*>(k2h_smem_raw);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    K2HubWarp& W = H.w[wid];
+    const int nh = *nhubs;
+    for (;;) {
+        if (threadIdx.x == 0) H.hub = atomicAdd(work, 1);
+        __syncthreads();
+        const int h = H.hub;
+        if (h >= nh) break;
+        const int u = hubs[h];
+        const int A = rp_or[u], B = rp_or[u + 1], len = B - A;
+        const bool staged = len <= kHubMax;
+        for (int i = threadIdx.x; i < kHubFilterWords; i += blockDim.x) H.filt[i] = 0u;
+        __syncthreads();
+        for (int i = threadIdx.x; i < len; i += blockDim.x) {
+            const int x = col_or[A + i];
+            if (staged) {
+                H.list[i] = x;
+                H.cnt[i] = 0;
+            }
+            const unsigned hh = hub_hash(x);
+            atomicOr(&H.filt[hh >> 5], 1u << (hh & 31));
+        }
+        __syncthreads();
+        for (int r0 = A + 32 * wid; r0 < B; r0 += 32 * kK2Warps) {
+            const int s = r0 + lane;
+            int wt = 0, vs = 0, vd = 0;
+            if (s < B) {
+                const int v = staged ? H.list[s - A] : col_or[s];
+                vs = rp_or[v];
+                vd = rp_or[v + 1] - vs;
+                wt = (vd + kQuad - 1) / kQuad;
+            }
+            const int incl = warp_incl_scan(wt, lane);
+            const int total = __shfl_sync(FULL, incl, 31);
+            const int pre = incl - wt;
+            W.pre[lane] = pre;
+            W.vst[lane] = vs;
+            W.vln[lane] = vd;
+            const unsigned nz = __ballot_sync(FULL, wt > 0);
+            int cur = nz ? __ffs(nz) - 1 : 0;
+            int head = 0, tail = 0;
+            __syncwarp();
+            for (int k0 = 0; k0 < total; k0 += 32) {
+                const bool starts = wt > 0 && pre >= k0 && pre < k0 + 32;
+                if (starts) W.owner[pre - k0] = lane;
+                const unsigned bits = __reduce_or_sync(FULL, starts ? (1u << (pre - k0)) : 0u);
+                __syncwarp();
+                const unsigned mine = bits & ((2u << lane) - 1u);
+                const int jj = mine ? W.owner[31 - __clz(mine)] : cur;
+                const int k = k0 + lane;
+                int i0 = 0;
+                unsigned cm = 0;
+                if (k < total) {
+                    i0 = (k - W.pre[jj]) * kQuad;
+                    const int sv0 = W.vst[jj] + i0;
+                    const int nval = min(kQuad, W.vln[jj] - i0);
+#pragma unroll
+                    for (int e = 0; e < kQuad; ++e) {
+                        if (e < nval) {
+                            const unsigned hh = hub_hash(col_or[sv0 + e]);
+                            if ((H.filt[hh >> 5] >> (hh & 31)) & 1u) cm |= 1u << e;
+                        }
+                    }
+                }
+                const int cbase = (jj << 16) | i0;
+#pragma unroll
+                for (int e = 0; e < kQuad; ++e) {
+                    const bool c = (cm >> e) & 1u;
+                    const unsigned b = __ballot_sync(FULL, c);
+                    if (c) W.ring[(tail + __popc(b & lt_mask)) & (kRing - 1)] = cbase + e;
+                    tail += __popc(b);
+                }
+                cur = __shfl_sync(FULL, jj, 31);
+                __syncwarp();
+                while (tail - head > 0 && (tail - head >= 32 || k0 + 32 >= total)) {
+                    const int cnt = min(32, tail - head);
+                    if (lane < cnt) {
+                        const int e = W.ring[(head + lane) & (kRing - 1)];
+                        const int j = e >> 16;
+                        const int sv = W.vst[j] + (e & 0xffff);  // slot of v -> w
+                        const int w = col_or[sv];
+                        const int* L = staged ? H.list : col_or + A;
+                        const int q = staged ? lower_bound_bl(L, len, w) : lower_bound(L, len, w);
+                        if (q < len && L[q] == w) {
+                            if (staged) {
+                                atomicAdd(&H.cnt[q], 1);             // t(u, w)
+                                atomicAdd(&H.cnt[r0 + j - A], 1);    // t(u, v)
+                            } else {
+                                atomicAdd(&t_or[A + q], 1);
+                                atomicAdd(&t_or[r0 + j], 1);
+                            }
+                            atomicAdd(&t_or[sv], 1);                 // t(v, w)
+                        }
+                    }
+                    head += cnt;
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        if (staged)
+            for (int i = threadIdx.x; i < len; i += blockDim.x) {
+                const int c = H.cnt[i];
+                if (c) atomicAdd(&t_or[A + i], c);
+            }
+        __syncthreads();
     }
 }
 
@@ -650,7 +808,7 @@ struct ScoreWs {
     unsigned *obits, *ubits;
     int2* vinfo;
     unsigned short* dslot;
-    int *col_or, *t_or, *work;
+    int *col_or, *t_or, *work, *hubs, *nhubs;
 };
 
 static ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
@@ -672,7 +830,9 @@ static ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
     w.t_or = cv.take<int>(m);
     w.vinfo = cv.take<int2>(n);
     w.dslot = cv.take<unsigned short>(2 * m);
-    w.work = cv.take<int>(1);
+    w.work = cv.take<int>(2);  // [0] K2 pivot queue, [1] K2h hub queue
+    w.hubs = cv.take<int>(n);
+    w.nhubs = cv.take<int>(1);
     return w;
 }
 
@@ -718,7 +878,8 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     }
     tile_first_rows(w.eoff, (int)n, m, w.trow, s);
     cudaMemsetAsync(w.t_or, 0, sizeof(int) * (size_t)m, s);
-    cudaMemsetAsync(w.work, 0, sizeof(int), s);
+    cudaMemsetAsync(w.work, 0, 2 * sizeof(int), s);
+    cudaMemsetAsync(w.nhubs, 0, sizeof(int), s);
     // a3: oriented intersection
     {
         const size_t smem = kK2Warps * sizeof(K2WarpSmem);
@@ -732,7 +893,18 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         record(ev, 1, s);
         k2_intersect<<<sms * occ, kK2Warps * 32, smem, s>>>(n, w.rp_or, w.col_or, w.t_or,
                                                              w.work);
-        count_launches(1);
+        // hub pivots: found after K1, processed one per CTA (no work and an early exit when
+        // the graph has none)
+        k2_find_hubs<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, w.rp_or, w.hubs, w.nhubs);
+        static int hub_set = 0;
+        const size_t hsmem = sizeof(K2HubSmem);
+        if (!hub_set) {
+            cudaFuncSetAttribute(k2_hubs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+            hub_set = 1;
+        }
+        k2_hubs<<<sms * 2, kK2Warps * 32, hsmem, s>>>(w.rp_or, w.col_or, w.hubs, w.nhubs,
+                                                       w.work + 1, w.t_or);
+        count_launches(3);
         record(ev, 2, s);
     }
     // a4: canonical gather + wedge + TW

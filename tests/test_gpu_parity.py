@@ -104,6 +104,22 @@ def test_hub_closed_forms(rb):
     assert st.tolist() == [[g.m, 1], [g.m, 1], [0, g.n]]
 
 
+def test_hub_beyond_smem_staging():
+    """K_8300: the top pivots' oriented lists (up to 8,299) exceed the hub kernel's 8,192-entry
+    smem staging, so their candidates are verified in global memory (closed form t = n - 2)."""
+    g = gg.complete(8300, np.int64)
+    t, w, tw = gpu_score(g)
+    assert t.size == 8300 * 8299 // 2
+    assert (t == 8298).all() and (w == 0).all() and (tw == 8298).all()
+
+
+def test_hub_pivots_with_community_structure(oracle_mod):
+    """Dense planted partition (blocks of 600, p_in 0.9): many pivots with |N+(u)| in
+    (256, 600] -- the hub kernel's staged path -- against the oracle."""
+    g = gg.planted_partition(3, 600, 0.9, 0.01, seed=9)
+    assert_score_parity(oracle_mod, g)
+
+
 def test_sparse_rows_uncached_tiles(oracle_mod):
     """Tiles spanning more rows than the smem row caches hold: a perfect matching on 3 of
     every 3k ids plus isolated vertices (every tile of canonical ids / CSR slots covers
