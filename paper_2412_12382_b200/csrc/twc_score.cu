@@ -11,6 +11,7 @@
 // The paper's own method (a full-list merge per edge, O(sum d^2) work) is replaced by
 // the oriented count (O(m * arboricity) work); the paper rejected it only for its per-worker
 // count arrays, which one int32 array plus atomics avoids on a GPU.  DESIGN.md Sec. 4.
+#include <algorithm>
 #include <climits>
 
 #include "twc_common.cuh"
@@ -366,7 +367,7 @@ __device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int head, int
     }
 }
 
-__global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n,
+__global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n, int chunk,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
                                                               int* __restrict__ t_or,
@@ -378,10 +379,10 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n,
     K2WarpSmem& S = smem[wid];
     for (;;) {
         int base = 0;
-        if (lane == 0) base = atomicAdd(work, kPivotChunk);
+        if (lane == 0) base = atomicAdd(work, chunk);
         base = __shfl_sync(FULL, base, 0);
         if (base >= n) break;
-        const int gend = (int)min((int64_t)base + kPivotChunk, n);
+        const int gend = (int)min((int64_t)base + chunk, n);
         int u = base;
         while (u < gend) {
             // ---- form a group of pivots [u, u+np) with <= kGroupSlots slots
@@ -891,7 +892,11 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
             if (occ < 1) occ = 1;
         }
         record(ev, 1, s);
-        k2_intersect<<<sms * occ, kK2Warps * 32, smem, s>>>(n, w.rp_or, w.col_or, w.t_or,
+        // pivots per queue grab: kPivotChunk, fewer when there are too few pivots to give every
+        // warp several grabs (small dense graphs), so the queue still balances the load
+        const int64_t warps = (int64_t)sms * occ * kK2Warps;
+        const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(kPivotChunk, n / (8 * warps)));
+        k2_intersect<<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or, w.t_or,
                                                              w.work);
         // hub pivots: found after K1, processed one per CTA (no work and an early exit when
         // the graph has none)
