@@ -4,12 +4,12 @@
 # exited 0 (ncu only profiles a command that has just run cleanly without it).
 # usage: bash scripts/gpu_iter.sh TAG [KERNEL_REGEX] [SKIP] [COUNT]
 TAG=${1:-iter}
-KRE=${2:-"k1_bits|k1_write|k2_intersect|k3_score|k_band_place|k_hook_list|k_finalize"}
+KRE=${2:-"k1_bits|k1_write|k2_intersect|k3_score|k_band_place|k_hook_list|k_finalize|k_part_edges"}
 SKIP=${3:-3}
 CNT=${4:-8}
 mkdir -p gpurun_out
 set -x
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_${TAG}.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_${TAG}.log 2>&1
 rc=$?; echo pytest_exit=$rc
 tail -5 gpurun_out/pytest_${TAG}.log
 [ $rc -eq 0 ] || exit $rc
