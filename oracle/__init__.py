@@ -14,6 +14,7 @@ this file only builds/loads it with ctypes and marshals numpy arrays.
     partition_stats(g, labels)   -> (n_communities, largest, intra_edges, sum_D2, modularity)
     sweep_report(g, tw, deltas)  -> per-delta points (kept, #CC, largest, E_in, sum_D2, Q)
     select(deltas, largest, n, modularity, jump_factor=0.1) -> (index, rule)
+    k4(g)                        -> int64[m] 4-cliques containing each canonical edge
 
 Every function is pinned in tests/test_oracle_pins.py against brute force, closed forms,
 invariants and library routines (scipy / networkx); see DESIGN.md "Oracle pins".
@@ -61,6 +62,8 @@ def _load():
         lib.oracle_partition_stats.restype = ctypes.c_int
         lib.oracle_select.argtypes = [ctypes.c_int32, P, P, I64, P, ctypes.c_double, P]
         lib.oracle_select.restype = ctypes.c_int32
+        lib.oracle_k4.argtypes = [I64, P, P, P]
+        lib.oracle_k4.restype = ctypes.c_int
         lib.oracle_max_threads.restype = ctypes.c_int
         lib.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = lib
@@ -187,3 +190,15 @@ def sweep_report(g, tw, deltas):
         pts.append({"delta": float(d), "kept": kept, "n_cc": nc, "largest": largest,
                     "intra": intra, "sum_d2": sd2, "modularity": q})
     return pts
+
+
+def k4(g):
+    """K4 participation per canonical edge (Table 1), int64[m]."""
+    lib = _load()
+    rowptr, colidx = _csr(g)
+    m = int(rowptr[-1]) // 2 if g.n > 0 else 0
+    out = np.zeros(m, dtype=np.int64)
+    if m:
+        if lib.oracle_k4(g.n, _ptr(rowptr), _ptr(colidx), _ptr(out)):
+            raise MemoryError("oracle_k4 allocation failed")
+    return out

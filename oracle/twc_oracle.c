@@ -35,6 +35,11 @@
  *                     one community) and the sum of d_u d_v over them is sum_c D_c^2 (D_c = total
  *                     degree of community c), so Q = (4 m E_in - sum_c D_c^2) / (4 m^2), one
  *                     IEEE division of two exactly represented integers.
+ *   oracle_k4      -- kappa-clique participation for kappa = 4 (Table 1; "we only
+ *                     consider K_4"): for every canonical edge (u, v), the number of
+ *                     4-cliques containing it = the number of pairs {w, x} of common neighbours
+ *                     (w < x, both in N(u) & N(v)) that are adjacent, checked by binary search
+ *                     in the sorted list N(w).  int64 per edge.
  *   oracle_select  -- the two rules of thumb of P:898-900 (reading C22): on the
  *                     decreasing-delta scan, the largest single-step increase of the normalised
  *                     largest-component size; if it is >= jump_factor return the higher delta
@@ -295,4 +300,59 @@ int32_t oracle_select(int32_t k, const double *deltas, const int64_t *largest, i
     *rule = 1;
     free(ord);
     return best;
+}
+
+static int has_edge(const int64_t *rowptr, const int32_t *colidx, int32_t a, int32_t b) {
+    int64_t lo = rowptr[a], hi = rowptr[a + 1];
+    while (lo < hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        if (colidx[mid] < b) lo = mid + 1; else hi = mid;
+    }
+    return lo < rowptr[a + 1] && colidx[lo] == b;
+}
+
+/* K4(u, v) for every canonical edge ("for each common neighbor pair w<x in
+ * N(u)&N(v), count if (w,x) is an edge").  Returns 0, or 1 when an allocation fails. */
+int oracle_k4(int64_t n, const int64_t *rowptr, const int32_t *colidx, int64_t *k4) {
+    if (n <= 0) return 0;
+    int64_t *eoff = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    if (!eoff) return 1;
+    canonical_offsets(n, rowptr, colidx, eoff);
+    int64_t dmax = 0;
+    for (int64_t u = 0; u < n; ++u)
+        if (rowptr[u + 1] - rowptr[u] > dmax) dmax = rowptr[u + 1] - rowptr[u];
+    int fail = 0;
+#pragma omp parallel
+    {
+        int32_t *common = (int32_t *)malloc(sizeof(int32_t) * (size_t)(dmax + 1));
+        if (!common) {
+#pragma omp atomic write
+            fail = 1;
+        }
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t u = 0; u < n; ++u) {
+            if (!common) continue;
+            int64_t c = eoff[u];
+            for (int64_t p = rowptr[u]; p < rowptr[u + 1]; ++p) {
+                int32_t v = colidx[p];
+                if (v <= u) continue;
+                /* common neighbours by one merge of the sorted lists */
+                int64_t i = rowptr[u], ie = rowptr[u + 1], j = rowptr[v], je = rowptr[v + 1];
+                int64_t nc = 0;
+                while (i < ie && j < je) {
+                    if (colidx[i] == colidx[j]) { common[nc++] = colidx[i]; ++i; ++j; }
+                    else if (colidx[i] < colidx[j]) ++i;
+                    else ++j;
+                }
+                int64_t cnt = 0;
+                for (int64_t a = 0; a < nc; ++a)
+                    for (int64_t b = a + 1; b < nc; ++b)
+                        cnt += has_edge(rowptr, colidx, common[a], common[b]);
+                k4[c++] = cnt;
+            }
+        }
+        free(common);
+    }
+    free(eoff);
+    return fail;
 }

@@ -63,3 +63,19 @@ def components_bfs(n, pairs):
                     lab[y] = s
                     stack.append(y)
     return np.asarray(lab, dtype=np.int32)
+
+
+def edge_k4(g):
+    """4-cliques per edge by enumerating every 4-subset of vertices (tiny graphs only)."""
+    import itertools
+    A = adjacency(g)
+    out = {}
+    for u in range(g.n):
+        for v in range(u + 1, g.n):
+            if A[u, v]:
+                out[(u, v)] = 0
+    for q in itertools.combinations(range(g.n), 4):
+        if all(A[a, b] for a, b in itertools.combinations(q, 2)):
+            for a, b in itertools.combinations(q, 2):
+                out[(a, b)] += 1
+    return out
