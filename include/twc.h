@@ -170,6 +170,19 @@ twc_status twc_sweep_f64(const twc_csr *g, const double *score, const double *de
                          int64_t *stats, void *stream);
 
 /* ---------------------------------------------------------------------------------------
+ * twc_score_k4 -- twc_score plus the kappa-clique participation for kappa = 4 (Table 1,
+ * P:417; "we only consider K_4"): k4[e] = number of 4-cliques containing the
+ * canonical edge e = number of adjacent pairs {w, x} of common neighbours of its endpoints
+ * (SURVEY 8(f) NEXT(4)).  t, wedge, tw: device int32[m] as twc_score; k4: device int64[m],
+ * canonical order.  Every 4-clique is counted once from its lowest (deg, id)-key vertex on the
+ * same oriented CSR (O(m * alpha^2) work).  Workspace: twc_score_k4_workspace_bytes(n, m, rb)
+ * (the score workspace followed by the K4 counters and scratch).
+ * ------------------------------------------------------------------------------------- */
+size_t twc_score_k4_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes);
+twc_status twc_score_k4(const twc_csr *g, void *workspace, size_t workspace_bytes, int32_t *t,
+                        int32_t *wedge, int32_t *tw, int64_t *k4, void *stream);
+
+/* ---------------------------------------------------------------------------------------
  * twc_partition_stats -- the statistics the threshold-selection study plots for each
  * partition ("norm # CC ... norm |largest CC|", modularity P:350-352; S:346;
  * SURVEY 8(f) NEXT(2)), for k partitions of the INPUT graph g at once.

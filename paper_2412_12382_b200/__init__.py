@@ -14,6 +14,7 @@ There is no CPU fallback: if libtwc.so is missing or no CUDA device is present, 
     counts, q         = twc_partition_stats(rowptr, colidx, labels)  # int64[k, 4], float64[k]
     index, rule       = twc_select_threshold(deltas, largest, q, n)  # host, rules of thumb
     report            = sweep_report(rowptr, colidx, deltas)         # the selection workflow
+    t, wedge, tw, k4  = twc_score_k4(rowptr, colidx)                 # + 4-clique participation
 
 rowptr: int32 or int64 tensor [n+1]; colidx: int32 tensor [2m] (CUDA tensors, except for
 twc_pipeline_host which takes CPU tensors, ideally pinned).  Outputs are in canonical edge
@@ -79,6 +80,8 @@ def load_library(path: str = LIB_PATH):
         "twc_score_sweep": (ctypes.c_int, [CP, P, I32, P, SZ, P, P, P, P, P, P, P]),
         "twc_similarity": (ctypes.c_int, [CP, P, I32, P, SZ, P, P]),
         "twc_sweep_f64": (ctypes.c_int, [CP, P, P, I32, P, SZ, P, P, P]),
+        "twc_score_k4_workspace_bytes": (SZ, [I64, I64, I32]),
+        "twc_score_k4": (ctypes.c_int, [CP, P, SZ, P, P, P, P, P]),
         "twc_partition_stats_workspace_bytes": (SZ, [I64, I64, I32]),
         "twc_partition_stats": (ctypes.c_int, [CP, P, I32, P, SZ, P, P, P]),
         "twc_select_threshold": (ctypes.c_int, [P, P, P, I32, I64, ctypes.c_double, P, P]),
@@ -396,3 +399,19 @@ def sweep_report(rowptr, colidx, deltas, tw=None, jump_factor=0.1, stream=None):
         i, rule = twc_select_threshold(deltas, [p["largest"] for p in pts], q, n, jump_factor)
         out.update(selected_index=i, selected_delta=float(deltas[i]), rule=rule)
     return out
+
+
+def twc_score_k4(rowptr, colidx, out=None, workspace=None, stream=None):
+    """twc_score plus K4 participation (Table 1): returns (t, wedge, tw, k4), k4 an
+    int64 tensor of 4-clique counts per canonical edge."""
+    lib = load_library()
+    g, n, m = _graph(rowptr, colidx)
+    dev = colidx.device
+    if out is None:
+        out = tuple(torch.empty(m, dtype=torch.int32, device=dev) for _ in range(3)) + (
+            torch.empty(m, dtype=torch.int64, device=dev),)
+    t, wedge, tw, k4 = out
+    ws = _workspace(lib.twc_score_k4_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    _check(lib.twc_score_k4(ctypes.byref(g), _ptr(ws), ws.numel(), _ptr(t), _ptr(wedge), _ptr(tw),
+                            _ptr(k4), _stream(stream)))
+    return t, wedge, tw, k4

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtwc.so")
 SOURCES = ["twc_scan.cu", "twc_score.cu", "twc_cluster.cu", "twc_similarity.cu", "twc_stats.cu",
-           "twc_api.cu"]
+           "twc_k4.cu", "twc_api.cu"]
 HEADERS = ["twc_common.cuh", "twc_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

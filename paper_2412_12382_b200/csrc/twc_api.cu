@@ -444,6 +444,34 @@ twc_status twc_validate_csr(const twc_csr* g, int32_t* verdict, void* stream) {
     return TWC_OK;
 }
 
+// ---- K4 participation (NEXT(4)) ----------------------------------------------------------
+size_t twc_score_k4_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes) {
+    (void)rowptr_bytes;
+    if (n < 0 || m < 0) return 0;
+    return score_ws_bytes(n, m) + k4_ws_bytes(n, m);
+}
+
+twc_status twc_score_k4(const twc_csr* g, void* ws, size_t ws_bytes, int32_t* t, int32_t* wedge,
+                        int32_t* tw, int64_t* k4, void* stream) {
+    g_err.clear();
+    twc_status st = check_csr(g);
+    if (st) return st;
+    if (g->m > 0 && (!t || !wedge || !tw || !k4)) return fail(TWC_EINVAL, "output array is NULL");
+    if (g->m == 0) return TWC_OK;
+    st = check_ws(ws, ws_bytes, score_ws_bytes(g->n, g->m) + k4_ws_bytes(g->n, g->m));
+    if (st) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    long long* k = reinterpret_cast<long long*>(k4);
+    if (g->rowptr_bytes == 4)
+        e = score_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx, ws,
+                            ws_bytes, t, wedge, tw, s, nullptr, nullptr, k);
+    else
+        e = score_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr), g->colidx,
+                                  ws, ws_bytes, t, wedge, tw, s, nullptr, nullptr, k);
+    return cuda_status(e, "twc_score_k4");
+}
+
 // ---- threshold selection (NEXT(2)) -------------------------------------------------------
 size_t twc_partition_stats_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes) {
     (void)rowptr_bytes;

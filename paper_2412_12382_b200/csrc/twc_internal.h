@@ -81,10 +81,20 @@ struct BinSpec {
     unsigned short* kband;  // device [m] band of kept[i]
 };
 size_t score_ws_bytes(int64_t n, int64_t m);
+// k4: NULL, or device int64[m] that receives the K4 participation of every canonical edge
+// (then ws must also hold k4_ws_bytes(n, m) after the score workspace)
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
-                       cudaEvent_t* ev = nullptr, const BinSpec* bin = nullptr);
+                       cudaEvent_t* ev = nullptr, const BinSpec* bin = nullptr,
+                       long long* k4 = nullptr);
+
+// ---- K4 participation (twc_k4.cu) -----------------------------------------------------------
+int k4_big_warps();
+size_t k4_ws_bytes(int64_t n, int64_t m);
+// counts per oriented slot (64-bit) into a buffer carved from ws; *k4_or_out points at it
+cudaError_t k4_count(int64_t n, int64_t m, const int* rp_or, const int* col_or, void* ws,
+                     size_t ws_bytes, unsigned long long** k4_or_out, cudaStream_t s);
 
 // ---- cluster (twc_cluster.cu) --------------------------------------------------------------
 size_t cluster_ws_bytes(int64_t n, int64_t m);

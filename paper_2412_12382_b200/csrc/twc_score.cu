@@ -691,7 +691,7 @@ __device__ __forceinline__ int sector_search(const int* __restrict__ col_or, int
 constexpr int kK3Threads = 256;
 constexpr int kMaxTileRows = 2048;
 
-template <typename RP, bool BIN>
+template <typename RP, bool BIN, bool K4 = false>
 __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     int64_t n, int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int2* __restrict__ vinfo, const unsigned short* __restrict__ dslot,
@@ -699,7 +699,8 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     const int* __restrict__ trow,
     const int* __restrict__ col_or, const int* __restrict__ opre,
     const unsigned* __restrict__ obits, const int* __restrict__ t_or, int* __restrict__ t,
-    int* __restrict__ wedge, int* __restrict__ tw, BinSpec bin) {
+    int* __restrict__ wedge, int* __restrict__ tw, BinSpec bin,
+    const unsigned long long* __restrict__ k4_or = nullptr, long long* __restrict__ k4 = nullptr) {
     constexpr int kIt = kTile / kK3Threads;
     __shared__ int s_off[kMaxTileRows + 1];
     extern __shared__ __align__(8) unsigned char k3_dyn[];  // BIN: thr[k] (i64), hist[k]
@@ -755,6 +756,7 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
                 sl = sector_search(col_or, vi.x, vi.y, u, n);
             }
             const int tt = t_or[sl];
+            if (K4) __stcs(k4 + c, (long long)k4_or[sl]);
             const int score = 3 * tt - du - dv + 2;
             __stcs(t + c, tt);
             __stcs(wedge + c, du + dv - 2 * tt - 2);
@@ -853,7 +855,7 @@ static int grid_for(int64_t items, int per_block, int max_blocks) {
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
-                       cudaEvent_t* ev, const BinSpec* bin) {
+                       cudaEvent_t* ev, const BinSpec* bin, long long* k4) {
     if (m == 0 || n == 0) return cudaGetLastError();
     Carver cv(ws, ws_bytes);
     ScoreWs w = carve_score(cv, n, m);
@@ -912,11 +914,23 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         count_launches(3);
         record(ev, 2, s);
     }
+    // NEXT(4): K4 participation on the same oriented CSR (workspace after the score's)
+    unsigned long long* k4_or = nullptr;
+    if (k4) {
+        const size_t used = score_ws_bytes(n, m);
+        cudaError_t e = k4_count(n, m, w.rp_or, w.col_or, static_cast<char*>(ws) + used,
+                                 ws_bytes - used, &k4_or, s);
+        if (e != cudaSuccess) return e;
+    }
     // a4: canonical gather + wedge + TW
     {
         const int64_t nt = num_tiles(m);
         const int grid = grid_for(nt, 1, sms * 8);
-        if (bin)
+        if (k4)
+            k3_score<RP, false, true><<<grid, kK3Threads, 0, s>>>(
+                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre,
+                w.obits, w.t_or, t, wedge, tw, BinSpec{}, k4_or, k4);
+        else if (bin)
             k3_score<RP, true><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
                 n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
                 wedge, tw, *bin);
@@ -932,9 +946,9 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
 
 template cudaError_t score_impl<int>(int64_t, int64_t, const int*, const int*, void*, size_t,
                                      int*, int*, int*, cudaStream_t, cudaEvent_t*,
-                                     const BinSpec*);
+                                     const BinSpec*, long long*);
 template cudaError_t score_impl<long long>(int64_t, int64_t, const long long*, const int*,
                                            void*, size_t, int*, int*, int*, cudaStream_t,
-                                           cudaEvent_t*, const BinSpec*);
+                                           cudaEvent_t*, const BinSpec*, long long*);
 
 }  // namespace twc
