@@ -401,6 +401,10 @@ def sweep_report(rowptr, colidx, deltas, tw=None, jump_factor=0.1, stream=None):
     return out
 
 
+def twc_score_k4_workspace_bytes(n, m, rowptr_bytes=4):
+    return int(load_library().twc_score_k4_workspace_bytes(n, m, rowptr_bytes))
+
+
 def twc_score_k4(rowptr, colidx, out=None, workspace=None, stream=None):
     """twc_score plus K4 participation (Table 1): returns (t, wedge, tw, k4), k4 an
     int64 tensor of 4-clique counts per canonical edge."""

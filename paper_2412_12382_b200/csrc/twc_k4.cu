@@ -207,9 +207,16 @@ cudaError_t k4_count(int64_t n, int64_t m, const int* rp_or, const int* col_or, 
     cudaMemsetAsync(k4_or, 0, sizeof(unsigned long long) * (size_t)m, s);
     cudaMemsetAsync(ctr, 0, 4 * sizeof(int), s);
     const int sms = num_sms();
-    const int64_t warps = (int64_t)sms * 2 * kK4Warps;
+    // one resident wave: the warps are latency-bound (a global round trip per slot and per
+    // triangle), so occupancy is what hides the latency
+    static int occ = 0;
+    if (occ == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_small, kK4Warps * 32, 0);
+        if (occ < 1) occ = 1;
+    }
+    const int64_t warps = (int64_t)sms * occ * kK4Warps;
     const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(16, n / (8 * warps)));
-    k4_small<<<sms * 2, kK4Warps * 32, 0, s>>>(n, chunk, rp_or, col_or, k4_or, ctr);
+    k4_small<<<sms * occ, kK4Warps * 32, 0, s>>>(n, chunk, rp_or, col_or, k4_or, ctr);
     k4_find_big<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rp_or, big, ctr + 1);
     k4_big<<<k4_big_warps() / 4, 128, 0, s>>>(big, ctr + 1, rp_or, col_or, k4_or, scratch,
                                                (int)cmax, ctr + 2);
