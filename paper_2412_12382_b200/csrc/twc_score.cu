@@ -447,24 +447,19 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n, int 
                     const unsigned mine = bits & ((2u << lane) - 1u);
                     const int jj = mine ? S.owner[31 - __clz(mine)] : cur;
                     const int k = k0 + lane;
+                    // branch-free: lanes past the end get nval = 0 and an empty mask
+                    const int i0 = (k - S.pre[jj]) * kQuad;  // first entry of the quad in N+(v)
+                    const int sv0 = S.vst[jj] + i0;
+                    const int nval = (k < total) ? min(kQuad, S.vln[jj] - i0) : 0;
                     int w[kQuad];
-                    int sv0 = 0, nval = 0, i0 = 0;
+#pragma unroll
+                    for (int e = 0; e < kQuad; ++e) w[e] = (e < nval) ? col_or[sv0 + e] : 0;
                     unsigned cm = 0;
-                    if (k < total) {
-                        i0 = (k - S.pre[jj]) * kQuad;  // first entry of the quad in N+(v)
-                        sv0 = S.vst[jj] + i0;
-                        nval = min(kQuad, S.vln[jj] - i0);
 #pragma unroll
-                        for (int e = 0; e < kQuad; ++e) w[e] = (e < nval) ? col_or[sv0 + e] : 0;
-                        if (staged) {
-#pragma unroll
-                            for (int e = 0; e < kQuad; ++e) {
-                                const unsigned h = filter_hash(w[e]);
-                                if (e < nval && ((S.filt[h >> 5] >> (h & 31)) & 1u)) cm |= 1u << e;
-                            }
-                        } else {
-                            cm = (1u << nval) - 1u;
-                        }
+                    for (int e = 0; e < kQuad; ++e) {
+                        const unsigned h = filter_hash(w[e]);
+                        const unsigned bit = (S.filt[h >> 5] >> (h & 31)) & 1u;
+                        cm |= (bit & (unsigned)(e < nval)) << e;
                     }
                     // append the candidates to the ring as (lane of the slot, index in N+(v))
                     const int cbase = (jj << 16) | i0;
