@@ -445,7 +445,8 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n, int 
                         __reduce_or_sync(FULL, starts ? (1u << (pre - k0)) : 0u);
                     __syncwarp();
                     const unsigned mine = bits & ((2u << lane) - 1u);
-                    const int jj = mine ? S.owner[31 - __clz(mine)] : cur;
+                    const int own = S.owner[31 - __clz(mine | 1u)];  // unconditional (no branch)
+                    const int jj = mine ? own : cur;
                     const int k = k0 + lane;
                     // branch-free: lanes past the end get nval = 0 and an empty mask
                     const int i0 = (k - S.pre[jj]) * kQuad;  // first entry of the quad in N+(v)
