@@ -298,76 +298,125 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
 // Warp-level scheme (persistent grid, chunked atomic pivot queue):
 //  * a warp groups consecutive pivots whose oriented lists total <= kGroupSlots slots and
 //    stages those lists (one contiguous range [A, B) of col_or) in shared memory, together
-//    with a kFilterBits-bit hash filter of their entries; a single pivot with a longer list is
-//    processed in place from global memory (no filter);
-//  * the group's slots are taken 32 at a time (one per lane); slot u->v owns the items
-//    w in N+(v) if d+(u) >= 2, cut into quads of kQuad consecutive entries.  The quads of the
-//    32 slots are flattened across the lanes (exclusive scan of the quad counts; the segment
-//    owning a quad is found with one __reduce_or_sync bit mask + one smem lookup), so each
-//    lane reads kQuad consecutive entries of one N+(v) and a warp reads a contiguous run;
-//  * an item whose w misses the filter cannot be in N+(u) (the common case); the others are
-//    appended to a per-warp ring of candidates, verified 32 at a time by binary search in the
-//    staged sorted list N+(u), so the search runs on full warps;
-//  * a verified hit adds 1 to t(u,w) and t(u,v) in per-warp smem counters (flushed once per
-//    group) and 1 to t(v,w) with one global reduction.
+//    with a kFilterBits-bit hash filter of their entries (pivots with longer lists are hubs,
+//    left to K2h);
+//  * the group's slots are taken 32 at a time (one per lane, a "round"); slot u->v owns the
+//    items w in N+(v) if d+(u) >= 2, cut into quads of kQuad consecutive entries.  The quads of
+//    the 32 slots are flattened across the lanes (exclusive scan of the quad counts; the
+//    segment owning a quad is found with one __reduce_or_sync bit mask + one smem lookup), so
+//    each lane reads kQuad consecutive entries of one N+(v) and a warp reads a contiguous run.
+//    The per-lane segment record {start - 4 * first quad, end, tag} gives a quad's slots with
+//    one 16-byte smem load; loads are clamped into the list, so loads and hashes run
+//    unpredicated and one validity mask is applied per quad;
+//  * filter position of w: word = top bits of x = w * K, bit = x & 31 (K odd, so x & 31 is a
+//    bijection of w & 31); one funnel rotate by (x - e) puts item e's bit at position e;
+//  * an item whose w misses the filter cannot be in N+(u) (the common case).  A lane with
+//    candidates pushes ONE record (slot of the quad, 4-bit mask, tag = slot u->v and pivot)
+//    with one ballot; records are expanded into a candidate ring 32 at a time and candidates
+//    verified 32 at a time by binary search in the staged sorted N+(u), so the prefix work and
+//    the search run on full warps.  Record and candidate entries are self-contained, so the
+//    rings carry over between the rounds of a group and drain only when full or at its end;
+//  * a verified hit adds 1 to t(u,w) and t(u,v) in per-warp byte counters (a count found from
+//    one pivot is at most |N+(u)| - 1 <= 255; flushed once per group) and 1 to t(v,w) with one
+//    global reduction;
+//  * the round setup prefetches each lane's N+(v) into L2, so the quad loop's loads find it.
+// DESIGN.md Sec. 4.1 lists the variants measured on the way (ncu evidence per step).
 constexpr int kK2Warps = 8;
 constexpr int kGroupSlots = 256;
-constexpr int kFilterBits = 4096;
+constexpr int kFilterLog = 13;
+constexpr int kFilterBits = 1 << kFilterLog;
 constexpr int kFilterWords = kFilterBits / 32;
 constexpr int kPivotChunk = 32;
 constexpr int kQuad = 4;
-constexpr int kRing = 256;  // >= 31 + 32 * kQuad pending candidates
+constexpr int kRing = 128;  // candidate ring (an expansion stops before it would overflow)
+constexpr int kRec = 64;    // record ring, >= 31 + 32 pending records
+constexpr unsigned kFiltK = 2654435761u;
 
+// 4,612 bytes per warp: 5 CTAs of 8 warps fit the 196 KB smem carveout and leave 60 KB of L1
+// for the N+(v) reads (a 228 KB carveout, i.e. 28 KB of L1, made the same kernel 18 % slower).
 struct K2WarpSmem {
-    int list[kGroupSlots];      // staged col_or[A, B)
-    int cnt[kGroupSlots];       // t(u,v)/t(u,w) counters for slots [A, B)
+    int list[kGroupSlots];          // staged col_or[A, B)
+    unsigned cnt[kGroupSlots / 4];  // byte counters t(u,v)/t(u,w) for slots [A, B)
     unsigned filt[kFilterWords];
-    int prp[33];                // group pivot offsets rp_or[u0 .. u0+np]
-    int pre[32];                // per-lane exclusive prefix of quad counts
-    int vst[32];                // start of N+(v) for the lane's slot
-    int vln[32];                // |N+(v)|
-    int plo[32];                // [plo, phi): oriented list of the lane's pivot (absolute slots)
-    int phi[32];
-    int owner[32];              // quad-segment owner lookup
-    int ring[kRing];            // candidates: (owning lane << 16) | index in N+(v)
+    int prp[33];                    // group pivot offsets rp_or[u0 .. u0+np]
+    int owner[32];                  // quad-segment owner lookup
+    int4 seg[32];                   // per lane: {start of N+(v) - 4 * first quad, end, tag, 0}
+    int2 ring[kRing];               // candidates: {slot of v -> w, tag}
+    int2 rec[kRec];                 // candidate quads: {slot of the quad, mask | tag << 4}
 };
 
-__device__ __forceinline__ unsigned filter_hash(int w) {
-    return ((unsigned)w * 2654435761u) >> (32 - 12);  // 12 bits = kFilterBits
+__device__ __forceinline__ unsigned filter_word(unsigned x) { return x >> (32 - kFilterLog + 5); }
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 // Verify ring entries [head, head + cnt) (cnt <= 32; lane i takes entry head + i).
-__device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int head, int cnt,
-                                          bool staged, int A, int r0,
+// tag = (slot of u -> v) - A | pivot index << 8.
+__device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int head, int cnt, int A,
                                           const int* __restrict__ col_or,
                                           int* __restrict__ t_or) {
     if (lane < cnt) {
-        const int e = S.ring[(head + lane) & (kRing - 1)];
-        const int jj = e >> 16;
-        const int sv = S.vst[jj] + (e & 0xffff);  // slot of v -> w
+        const int2 c = S.ring[(head + lane) & (kRing - 1)];
+        const int sv = c.x;  // slot of v -> w
         const int w = col_or[sv];
-        const int plo = S.plo[jj], len = S.phi[jj] - plo;
-        if (staged) {
-            const int* L = S.list + (plo - A);
-            const int q = lower_bound_bl(L, len, w);
-            if (q < len && L[q] == w) {
-                atomicAdd(&S.cnt[plo - A + q], 1);  // t(u, w)
-                atomicAdd(&S.cnt[r0 + jj - A], 1);  // t(u, v)
-                atomicAdd(&t_or[sv], 1);            // t(v, w)
-            }
-        } else {
-            const int* L = col_or + plo;
-            const int q = lower_bound(L, len, w);
-            if (q < len && L[q] == w) {
-                atomicAdd(&t_or[plo + q], 1);
-                atomicAdd(&t_or[r0 + jj], 1);
-                atomicAdd(&t_or[sv], 1);
-            }
+        const int pi = c.y >> 8, so = c.y & 255;
+        const int plo = S.prp[pi] - A, len = S.prp[pi + 1] - S.prp[pi];
+        const int* L = S.list + plo;
+        const int q = lower_bound_bl(L, len, w);
+        if (q < len && L[q] == w) {
+            const int i = plo + q;
+            atomicAdd(&S.cnt[i >> 2], 1u << (8 * (i & 3)));    // t(u, w)
+            atomicAdd(&S.cnt[so >> 2], 1u << (8 * (so & 3)));  // t(u, v)
+            atomicAdd(&t_or[sv], 1);                          // t(v, w)
         }
     }
 }
 
-__global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n, int chunk,
+// Expand records [rhead, rhead + cnt) (cnt <= 32, lane i takes record rhead + i) into the
+// candidate ring at tail while they fit; returns the number of records consumed (a prefix; at
+// least 24 when fewer than 32 candidates are pending).
+__device__ __forceinline__ int k2_expand(K2WarpSmem& S, int lane, int rhead, int cnt, int head,
+                                         int& tail) {
+    const int2 r = (lane < cnt) ? S.rec[(rhead + lane) & (kRec - 1)] : make_int2(0, 0);
+    const unsigned cm = (unsigned)r.y & 15u;
+    const int nc = __popc(cm);
+    const int incl = warp_incl_scan(nc, lane);
+    const bool fits = lane < cnt && incl <= kRing - (tail - head);
+    const unsigned fb = __ballot_sync(FULL, fits);
+    if (fits) {
+        int pos = tail + incl - nc;
+        const int tag = r.y >> 4;
+#pragma unroll
+        for (int e = 0; e < kQuad; ++e) {
+            if ((cm >> e) & 1u) {
+                S.ring[pos & (kRing - 1)] = make_int2(r.x + e, tag);
+                ++pos;
+            }
+        }
+    }
+    const int used = __popc(fb);
+    tail += __shfl_sync(FULL, incl, max(used - 1, 0)) * (used > 0);
+    return used;
+}
+
+// Drain: expand pending records while at least `keep` remain and verify full warps of
+// candidates.
+__device__ __forceinline__ void k2_drain(K2WarpSmem& S, int lane, int keep, int A, int& rhead,
+                                         int rtail, int& head, int& tail,
+                                         const int* __restrict__ col_or, int* __restrict__ t_or) {
+    while (rtail - rhead > keep) {
+        rhead += k2_expand(S, lane, rhead, min(32, rtail - rhead), head, tail);
+        __syncwarp();
+        while (tail - head >= 32) {
+            k2_verify(S, lane, head, 32, A, col_or, t_or);
+            head += 32;
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int chunk,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
                                                               int* __restrict__ t_or,
@@ -394,33 +443,30 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n, int 
                 ++u;
                 continue;
             }
-            const bool staged = true;
             const int np = __popc(fit);
             const int B = __shfl_sync(FULL, e_l, np - 1);
             if (lane == 0) S.prp[0] = A;
             if (lane < np) S.prp[lane + 1] = e_l;
-            if (staged) {
-                for (int i = lane; i < kFilterWords; i += 32) S.filt[i] = 0u;
-                __syncwarp();
-                for (int i = lane; i < B - A; i += 32) {
-                    const int x = col_or[A + i];
-                    S.list[i] = x;
-                    S.cnt[i] = 0;
-                    const unsigned h = filter_hash(x);
-                    atomicOr(&S.filt[h >> 5], 1u << (h & 31));
-                }
+            for (int i = lane; i < kFilterWords; i += 32) S.filt[i] = 0u;
+            for (int i = lane; i < kGroupSlots / 4; i += 32) S.cnt[i] = 0u;
+            __syncwarp();
+            for (int i = lane; i < B - A; i += 32) {
+                const int x = col_or[A + i];
+                S.list[i] = x;
+                const unsigned h = (unsigned)x * kFiltK;
+                atomicOr(&S.filt[filter_word(h)], 1u << (h & 31));
             }
             __syncwarp();
+            int head = 0, tail = 0;    // candidate ring
+            int rhead = 0, rtail = 0;  // record ring
             // ---- rounds of 32 slots
             for (int r0 = A; r0 < B; r0 += 32) {
                 const int s = r0 + lane;
-                int wt = 0, vs = 0, vd = 0, lo = 0, hi = 0;
+                int wt = 0, vs = 0, vd = 0, pi = 0;
                 if (s < B) {
-                    const int v = staged ? S.list[s - A] : col_or[s];
-                    const int pi = staged ? last_le(S.prp, np + 1, s) : 0;
-                    lo = S.prp[pi];
-                    hi = S.prp[pi + 1];
-                    if (hi - lo >= 2) {
+                    const int v = S.list[s - A];
+                    pi = last_le(S.prp, np + 1, s);
+                    if (S.prp[pi + 1] - S.prp[pi] >= 2) {
                         vs = rp_or[v];
                         vd = rp_or[v + 1] - vs;
                         wt = (vd + kQuad - 1) / kQuad;
@@ -429,14 +475,13 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n, int 
                 const int incl = warp_incl_scan(wt, lane);
                 const int total = __shfl_sync(FULL, incl, 31);
                 const int pre = incl - wt;
-                S.pre[lane] = pre;
-                S.vst[lane] = vs;
-                S.vln[lane] = vd;
-                S.plo[lane] = lo;
-                S.phi[lane] = hi;
+                S.seg[lane] = make_int4(vs - kQuad * pre, vs + vd, (s - A) | (pi << 8), 0);
+                if (wt > 0) {  // the quad loop below reads N+(v)
+                    prefetch_l2(col_or + vs);
+                    if (((vs + vd - 1) >> 5) != (vs >> 5)) prefetch_l2(col_or + vs + vd - 1);
+                }
                 const unsigned nz = __ballot_sync(FULL, wt > 0);
                 int cur = nz ? __ffs(nz) - 1 : 0;
-                int head = 0, tail = 0;  // candidate ring
                 __syncwarp();
                 for (int k0 = 0; k0 < total; k0 += 32) {
                     const bool starts = wt > 0 && pre >= k0 && pre < k0 + 32;
@@ -445,48 +490,39 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n, int 
                         __reduce_or_sync(FULL, starts ? (1u << (pre - k0)) : 0u);
                     __syncwarp();
                     const unsigned mine = bits & ((2u << lane) - 1u);
-                    const int own = S.owner[31 - __clz(mine | 1u)];  // unconditional (no branch)
+                    const int own = S.owner[31 - __clz(mine | 1u)];
+                    // lanes past the last quad belong to the last segment and get nval <= 0
                     const int jj = mine ? own : cur;
-                    const int k = k0 + lane;
-                    // branch-free: lanes past the end get nval = 0 and an empty mask
-                    const int i0 = (k - S.pre[jj]) * kQuad;  // first entry of the quad in N+(v)
-                    const int sv0 = S.vst[jj] + i0;
-                    const int nval = (k < total) ? min(kQuad, S.vln[jj] - i0) : 0;
+                    const int4 sg = S.seg[jj];
+                    const int sv0 = sg.x + kQuad * (k0 + lane);
+                    const int nval = sg.y - sv0;
                     int w[kQuad];
 #pragma unroll
-                    for (int e = 0; e < kQuad; ++e) w[e] = (e < nval) ? col_or[sv0 + e] : 0;
+                    for (int e = 0; e < kQuad; ++e) w[e] = __ldg(col_or + min(sv0 + e, sg.y - 1));
                     unsigned cm = 0;
 #pragma unroll
                     for (int e = 0; e < kQuad; ++e) {
-                        const unsigned h = filter_hash(w[e]);
-                        const unsigned bit = (S.filt[h >> 5] >> (h & 31)) & 1u;
-                        cm |= (bit & (unsigned)(e < nval)) << e;
+                        const unsigned x = (unsigned)w[e] * kFiltK;
+                        const unsigned word = S.filt[filter_word(x)];
+                        cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
                     }
-                    // append the candidates to the ring as (lane of the slot, index in N+(v))
-                    const int cbase = (jj << 16) | i0;
-#pragma unroll
-                    for (int e = 0; e < kQuad; ++e) {
-                        const bool c = (cm >> e) & 1u;
-                        const unsigned b = __ballot_sync(FULL, c);
-                        if (c) S.ring[(tail + __popc(b & lt_mask)) & (kRing - 1)] = cbase + e;
-                        tail += __popc(b);
-                    }
+                    cm &= (1u << min(max(nval, 0), kQuad)) - 1u;
+                    const unsigned hb = __ballot_sync(FULL, cm != 0u);
+                    if (cm) S.rec[(rtail + __popc(hb & lt_mask)) & (kRec - 1)] =
+                                make_int2(sv0, (int)cm | (sg.z << 4));
+                    rtail += __popc(hb);
                     cur = __shfl_sync(FULL, jj, 31);
                     __syncwarp();
-                    while (tail - head >= 32) {
-                        k2_verify(S, lane, head, 32, staged, A, r0, col_or, t_or);
-                        head += 32;
-                    }
-                    __syncwarp();
+                    k2_drain(S, lane, 31, A, rhead, rtail, head, tail, col_or, t_or);
                 }
-                if (tail > head) k2_verify(S, lane, head, tail - head, staged, A, r0, col_or, t_or);
-                __syncwarp();
+                __syncwarp();  // seg / owner are rewritten by the next round
             }
-            if (staged) {
-                for (int i = lane; i < B - A; i += 32) {
-                    const int c = S.cnt[i];
-                    if (c) atomicAdd(&t_or[A + i], c);
-                }
+            k2_drain(S, lane, 0, A, rhead, rtail, head, tail, col_or, t_or);
+            if (tail > head) k2_verify(S, lane, head, tail - head, A, col_or, t_or);
+            __syncwarp();
+            for (int i = lane; i < B - A; i += 32) {
+                const unsigned c = (S.cnt[i >> 2] >> (8 * (i & 3))) & 0xffu;
+                if (c) atomicAdd(&t_or[A + i], (int)c);
             }
             __syncwarp();
             u += np;
@@ -500,12 +536,13 @@ __global__ void __launch_bounds__(kK2Warps * 32, 4) k2_intersect(int64_t n, int 
 // flattened-quad scan, filter and candidate ring as K2.  A list longer than kHubMax keeps only
 // the filter; its candidates are verified by binary search in global memory.
 constexpr int kHubMax = 8192;
+constexpr int kHubRing = 256;  // >= 31 + 32 * kQuad pending candidates
 constexpr int kHubFilterLog = 16;
 constexpr int kHubFilterWords = (1 << kHubFilterLog) / 32;
 
 struct K2HubWarp {
     int pre[32], vst[32], vln[32], owner[32];
-    int ring[kRing];
+    int ring[kHubRing];
 };
 struct K2HubSmem {
     int list[kHubMax];
@@ -608,7 +645,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                 for (int e = 0; e < kQuad; ++e) {
                     const bool c = (cm >> e) & 1u;
                     const unsigned b = __ballot_sync(FULL, c);
-                    if (c) W.ring[(tail + __popc(b & lt_mask)) & (kRing - 1)] = cbase + e;
+                    if (c) W.ring[(tail + __popc(b & lt_mask)) & (kHubRing - 1)] = cbase + e;
                     tail += __popc(b);
                 }
                 cur = __shfl_sync(FULL, jj, 31);
@@ -616,7 +653,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                 while (tail - head > 0 && (tail - head >= 32 || k0 + 32 >= total)) {
                     const int cnt = min(32, tail - head);
                     if (lane < cnt) {
-                        const int e = W.ring[(head + lane) & (kRing - 1)];
+                        const int e = W.ring[(head + lane) & (kHubRing - 1)];
                         const int j = e >> 16;
                         const int sv = W.vst[j] + (e & 0xffff);  // slot of v -> w
                         const int w = col_or[sv];
