@@ -15,7 +15,9 @@ ia, isrc = hdr.index("Address"), hdr.index("Source")
 iex, ismp = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
 data = []
 for r in rows[2:]:
-    if len(r) <= iex:
+    if r and r[0] == "Kernel Name":  # next kernel of a multi-kernel page: keep the first only
+        break
+    if len(r) <= iex or r[ia] == "Address":
         continue
     data.append((int(r[ia], 16), r[isrc].strip(), int(r[iex] or 0), int(r[ismp] or 0)))
 base = data[0][0]
