@@ -125,6 +125,12 @@ class Clocks:
                 self.p.kill()
 
     def summary(self):
+        if getattr(self, "_summary", None) is not None:
+            return self._summary
+        self._summary = self._summarize()
+        return self._summary
+
+    def _summarize(self):
         self.f.flush()
         rows = []
         for line in open(self.f.name):
@@ -382,11 +388,23 @@ def main_b200(args):
     k2_avg_s = statistics.mean(k2_ms) / 1000.0
     peak, peak_src = measured_peak()
     achieved = k2_bytes / k2_avg_s / 1e9
-    traffic, _ = ncu_traffic()
+    traffic, k2prof = ncu_traffic()
     roofline = {"bound": "hbm", "kernel": "k2_intersect", "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": k2_bytes, "peak_source": peak_src,
                 "k2_ms_avg": 1000 * k2_avg_s}
+    if k2prof and k2prof.get("warp_inst_per_launch"):
+        # K2 is bound by instruction issue and load latency, not by DRAM:
+        # its warp instructions per launch (committed ncu capture) over the live K2 time,
+        # against 4 schedulers x SMs x max SM clock (one warp instruction per cycle each)
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        smax = clk.summary().get("sm_max_mhz") or 1965.0  # B200 max SM clock if unsampled
+        peak_ginst = 4 * sms * smax / 1000.0
+        ach_ginst = k2prof["warp_inst_per_launch"] / k2_avg_s / 1e9
+        roofline["issue"] = {"warp_inst_per_launch": k2prof["warp_inst_per_launch"],
+                             "achieved": ach_ginst, "peak": peak_ginst, "unit": "G warp-inst/s",
+                             "frac": ach_ginst / peak_ginst,
+                             "ncu_issue_active_pct": k2prof.get("issue_active_pct")}
 
     # ---- end to end through the public host API
     e2e = None

@@ -72,6 +72,8 @@ def full_summary(tag, rep):
             wr = to_bytes(r[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
             k2 = {"tag": tag, "dram_bytes_read": rd, "dram_bytes_write": wr,
                   "dram_bytes_per_launch": rd + wr,
+                  "warp_inst_per_launch": float(r[col["smsp__inst_executed.sum"]].replace(",", "")),
+                  "issue_active_pct": float(r[col["smsp__issue_active.avg.pct_of_peak_sustained_active"]]),
                   "duration": r[col["gpu__time_duration.sum"]] + " " + units[col["gpu__time_duration.sum"]],
                   "source": f"profiles/{tag}_ncu_full.md"}
     with open(os.path.join(PROF, f"{tag}_ncu_full.md"), "w") as f:
