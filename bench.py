@@ -359,6 +359,35 @@ def main_b200(args):
                 "sweep16_ms": statistics.mean(wev[i][0].elapsed_time(wev[i][2]) for i in range(Ks))}
     separate["step_ms"] = separate["score_ms"] + separate["sweep16_ms"]
 
+    # ---- the same fused step captured once in a CUDA graph and replayed (the library makes no
+    # host synchronisation and no host->device copy inside the call, so it is capturable)
+    graph = None
+    try:
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(stream)
+        cg = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs):
+            step()                              # warm on the capture stream
+            torch.cuda.synchronize()
+            with torch.cuda.graph(cg, stream=gs):
+                step()
+        torch.cuda.synchronize()
+        Kg = min(K, 20)
+        gse = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(Kg)]
+        for i in range(Kg):
+            flush.zero_()
+            gse[i][0].record(stream)
+            cg.replay()
+            gse[i][1].record(stream)
+        torch.cuda.synchronize()
+        g_ms = statistics.mean(a.elapsed_time(b) for a, b in gse)
+        graph = {"ms_per_step": g_ms, "value": m / (g_ms / 1000.0), "steps": Kg,
+                 "note": "twc_score_sweep captured in one CUDA graph, replayed; L2 flushed between"}
+        del cg
+    except Exception as exc:  # capture is reported, never required
+        graph = {"error": repr(exc)[:200]}
+
     # ---- NEXT(2): statistics of the k partitions + the selection rules (reported, not in value)
     ws_ps = torch.empty(max(1, twc.twc_partition_stats_workspace_bytes(n, m, rb)),
                         dtype=torch.uint8, device=dev)
@@ -472,7 +501,7 @@ def main_b200(args):
             "phases_ms": phases, "separate_calls_ms": separate, "selection": selection,
             "score_edges_per_s": world * m / (phases["score"] / 1000.0),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": csum, "wall_s_timed": wall,
+            "clocks": csum, "wall_s_timed": wall, "cuda_graph": graph,
             "graph": {"triangles": T, "sum_dminus_dplus": S, "max_dplus": dplus_max,
                       "max_degree": int(np.diff(g.rowptr.astype(np.int64)).max())}}
     if rank == 0:

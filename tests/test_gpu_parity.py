@@ -279,6 +279,47 @@ def test_fused_score_sweep_small(oracle_mod):
     fused_parity(oracle_mod, gg.complete(3000), [2998.0, 2999.0, 0.0])
 
 
+def test_fused_call_in_cuda_graph(oracle_mod):
+    # the fused call makes no host synchronisation and no host->device copy, so it can be
+    # captured in a CUDA graph; replays (after the inputs change in place) match the oracle
+    g = gg.config_graph(2)
+    rp, ci = harness.to_device(g, "cuda")
+    ot = oracle_mod.score(g)
+    deltas = harness.thresholds(2, ot[2])
+    k = len(deltas)
+    t, w, tw = (torch.empty(g.m, dtype=torch.int32, device="cuda") for _ in range(3))
+    labels = torch.empty((k, g.n), dtype=torch.int32, device="cuda")
+    stats = torch.empty((k, 2), dtype=torch.int64, device="cuda")
+    ws = torch.empty(twc.twc_score_sweep_workspace_bytes(g.n, g.m, rp.element_size()),
+                     dtype=torch.uint8, device="cuda")
+
+    def step():
+        twc.twc_score_sweep(rp, ci, deltas, out=(t, w, tw), labels=labels, stats=stats,
+                            workspace=ws)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    cg = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        step()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(cg, stream=s):
+            step()
+    torch.cuda.synchronize()
+    for _ in range(2):
+        t.fill_(-7); labels.fill_(-7); stats.fill_(-7)
+        cg.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(t.cpu().numpy(), ot[0])
+        assert np.array_equal(w.cpu().numpy(), ot[1])
+        assert np.array_equal(tw.cpu().numpy(), ot[2])
+        lab, st = labels.cpu().numpy(), stats.cpu().numpy()
+        for i, d in enumerate(deltas):
+            ol, kept, ncomp = oracle_mod.cluster(g, ot[2], d)
+            assert np.array_equal(lab[i], ol), d
+            assert (int(st[i, 0]), int(st[i, 1])) == (kept, ncomp), d
+
+
 # ------------------------------------------------------------------ the five configs, full size
 
 @pytest.mark.parametrize("config", [1, 2, 3, 4, 5])
