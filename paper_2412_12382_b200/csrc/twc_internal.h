@@ -83,11 +83,21 @@ struct BinSpec {
 size_t score_ws_bytes(int64_t n, int64_t m);
 // k4: NULL, or device int64[m] that receives the K4 participation of every canonical edge
 // (then ws must also hold k4_ws_bytes(n, m) after the score workspace)
+// shard: NULL, or {rank, world}: count only the triangles whose pivot (lowest-key vertex) lies in
+// the rank's pivot range and write only t (wedge, tw unused)
+struct ShardSpec {
+    int rank, world;
+};
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
                        cudaEvent_t* ev = nullptr, const BinSpec* bin = nullptr,
-                       long long* k4 = nullptr);
+                       long long* k4 = nullptr, const ShardSpec* shard = nullptr);
+// wedge = d_u + d_v - 2t - 2, TW = 3t - d_u - d_v + 2 from canonical t (cluster workspace)
+template <typename RP>
+cudaError_t finish_scores_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+                               const int* t, void* ws, size_t ws_bytes, int* wedge, int* tw,
+                               cudaStream_t s);
 
 // ---- K4 participation (twc_k4.cu) -----------------------------------------------------------
 int k4_big_warps();

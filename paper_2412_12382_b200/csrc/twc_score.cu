@@ -417,22 +417,25 @@ __device__ __forceinline__ void k2_drain(K2WarpSmem& S, int lane, int keep, int 
     }
 }
 
+// range: NULL (all pivots) or device {u_lo, u_hi} of a shard (the queue starts at u_lo)
 __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int chunk,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
                                                               int* __restrict__ t_or,
-                                                              int* __restrict__ work) {
+                                                              int* __restrict__ work,
+                                                              const int* __restrict__ range) {
     extern __shared__ __align__(16) unsigned char k2_smem_raw[];
     K2WarpSmem* smem = reinterpret_cast<K2WarpSmem*>(k2_smem_raw);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
     K2WarpSmem& S = smem[wid];
+    const int64_t u_end = range ? (int64_t)range[1] : n;
     for (;;) {
         int base = 0;
         if (lane == 0) base = atomicAdd(work, chunk);
         base = __shfl_sync(FULL, base, 0);
-        if (base >= n) break;
-        const int gend = (int)min((int64_t)base + chunk, n);
+        if (base >= u_end) break;
+        const int gend = (int)min((int64_t)base + chunk, u_end);
         int u = base;
         while (u < gend) {
             // ---- form a group of pivots [u, u+np) with <= kGroupSlots slots
@@ -531,6 +534,27 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
     }
 }
 
+// Pivot range of a shard: rank r of P takes the pivots u whose oriented lists
+// start in [r m / P, (r+1) m / P) -- contiguous vertex ranges with equal oriented-slot counts;
+// the ranges of the P ranks partition [0, n).  Also points the pivot queue at u_lo.
+__global__ void k2_shard_range(int64_t n, int64_t m, const int* __restrict__ rp_or, int rank,
+                               int world, int* __restrict__ range, int* __restrict__ work) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    auto first_ge = [&](int64_t target) -> int {  // first u in [0, n] with rp_or[u] >= target
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)rp_or[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        return (int)lo;
+    };
+    const int lo = rank == 0 ? 0 : first_ge(m * rank / world);
+    const int hi = rank == world - 1 ? (int)n : first_ge(m * (rank + 1) / world);
+    range[0] = lo;
+    range[1] = hi;
+    work[0] = lo;
+}
+
 // ------------------------------------------------------ K2h: hub pivots (|N+(u)| > 256)
 // One pivot per CTA: the whole block stages N+(u) (up to kHubMax entries) and a 64K-bit filter
 // of it in shared memory, and its 8 warps take the pivot's slots 32 at a time with the same
@@ -559,9 +583,10 @@ __device__ __forceinline__ unsigned hub_hash(int w) {
 
 // hubs[] = pivots with more than kGroupSlots oriented neighbours (order irrelevant)
 __global__ void k2_find_hubs(int64_t n, const int* __restrict__ rp_or, int* __restrict__ hubs,
-                             int* __restrict__ nhubs) {
+                             int* __restrict__ nhubs, const int* __restrict__ range) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool hub = u < n && rp_or[u + 1] - rp_or[u] > kGroupSlots;
+    const bool in = range ? (u >= range[0] && u < range[1]) : u < n;
+    const bool hub = in && rp_or[u + 1] - rp_or[u] > kGroupSlots;
     const unsigned b = __ballot_sync(FULL, hub);
     if (!b) return;
     const int lane = threadIdx.x & 31;
@@ -725,7 +750,7 @@ __device__ __forceinline__ int sector_search(const int* __restrict__ col_or, int
 constexpr int kK3Threads = 256;
 constexpr int kMaxTileRows = 2048;
 
-template <typename RP, bool BIN, bool K4 = false>
+template <typename RP, bool BIN, bool K4 = false, bool TONLY = false>
 __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     int64_t n, int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int2* __restrict__ vinfo, const unsigned short* __restrict__ dslot,
@@ -793,8 +818,10 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
             if (K4) __stcs(k4 + c, (long long)k4_or[sl]);
             const int score = 3 * tt - du - dv + 2;
             __stcs(t + c, tt);
-            __stcs(wedge + c, du + dv - 2 * tt - 2);
-            __stcs(tw + c, score);
+            if (!TONLY) {
+                __stcs(wedge + c, du + dv - 2 * tt - 2);
+                __stcs(tw + c, score);
+            }
             if (BIN && (long long)score >= s_thr[bin.k - 1]) {  // kept at the smallest threshold
                 bnd = band_of(score, s_thr, bin.k);
                 kp[it] = make_int2(u, v);
@@ -845,7 +872,7 @@ struct ScoreWs {
     unsigned *obits, *ubits;
     int2* vinfo;
     unsigned short* dslot;
-    int *col_or, *t_or, *work, *hubs, *nhubs;
+    int *col_or, *t_or, *work, *hubs, *nhubs, *range;
 };
 
 static ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
@@ -870,6 +897,7 @@ static ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
     w.work = cv.take<int>(2);  // [0] K2 pivot queue, [1] K2h hub queue
     w.hubs = cv.take<int>(n);
     w.nhubs = cv.take<int>(1);
+    w.range = cv.take<int>(2);
     return w;
 }
 
@@ -889,7 +917,8 @@ static int grid_for(int64_t items, int per_block, int max_blocks) {
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
-                       cudaEvent_t* ev, const BinSpec* bin, long long* k4) {
+                       cudaEvent_t* ev, const BinSpec* bin, long long* k4,
+                       const ShardSpec* shard) {
     if (m == 0 || n == 0) return cudaGetLastError();
     Carver cv(ws, ws_bytes);
     ScoreWs w = carve_score(cv, n, m);
@@ -917,6 +946,12 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     cudaMemsetAsync(w.t_or, 0, sizeof(int) * (size_t)m, s);
     cudaMemsetAsync(w.work, 0, 2 * sizeof(int), s);
     cudaMemsetAsync(w.nhubs, 0, sizeof(int), s);
+    const int* range = nullptr;  // a shard counts only the triangles of its pivot range
+    if (shard && shard->world > 1) {
+        k2_shard_range<<<1, 32, 0, s>>>(n, m, w.rp_or, shard->rank, shard->world, w.range, w.work);
+        count_launches(1);
+        range = w.range;
+    }
     // a3: oriented intersection
     {
         const size_t smem = kK2Warps * sizeof(K2WarpSmem);
@@ -933,10 +968,11 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         const int64_t warps = (int64_t)sms * occ * kK2Warps;
         const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(kPivotChunk, n / (8 * warps)));
         k2_intersect<<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or, w.t_or,
-                                                             w.work);
+                                                             w.work, range);
         // hub pivots: found after K1, processed one per CTA (no work and an early exit when
         // the graph has none)
-        k2_find_hubs<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, w.rp_or, w.hubs, w.nhubs);
+        k2_find_hubs<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, w.rp_or, w.hubs, w.nhubs,
+                                                                range);
         static int hub_set = 0;
         const size_t hsmem = sizeof(K2HubSmem);
         if (!hub_set) {
@@ -960,7 +996,11 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     {
         const int64_t nt = num_tiles(m);
         const int grid = grid_for(nt, 1, sms * 8);
-        if (k4)
+        if (shard)  // t only (partial counts of a shard)
+            k3_score<RP, false, false, true><<<grid, kK3Threads, 0, s>>>(
+                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre,
+                w.obits, w.t_or, t, wedge, tw, BinSpec{});
+        else if (k4)
             k3_score<RP, false, true><<<grid, kK3Threads, 0, s>>>(
                 n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre,
                 w.obits, w.t_or, t, wedge, tw, BinSpec{}, k4_or, k4);
@@ -980,9 +1020,10 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
 
 template cudaError_t score_impl<int>(int64_t, int64_t, const int*, const int*, void*, size_t,
                                      int*, int*, int*, cudaStream_t, cudaEvent_t*,
-                                     const BinSpec*, long long*);
+                                     const BinSpec*, long long*, const ShardSpec*);
 template cudaError_t score_impl<long long>(int64_t, int64_t, const long long*, const int*,
                                            void*, size_t, int*, int*, int*, cudaStream_t,
-                                           cudaEvent_t*, const BinSpec*, long long*);
+                                           cudaEvent_t*, const BinSpec*, long long*,
+                                           const ShardSpec*);
 
 }  // namespace twc
