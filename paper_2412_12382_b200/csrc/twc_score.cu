@@ -306,9 +306,11 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
 //    the 32 slots are flattened across the lanes (exclusive scan of the quad counts; the
 //    segment owning a quad is found with one __reduce_or_sync bit mask + one smem lookup), so
 //    each lane reads kQuad consecutive entries of one N+(v) and a warp reads a contiguous run.
-//    The per-lane segment record {start - 4 * first quad, end, tag} gives a quad's slots with
-//    one 16-byte smem load; loads are clamped into the list, so loads and hashes run
-//    unpredicated and one validity mask is applied per quad;
+//    Quads are 16-byte aligned groups of col_or covering [start & ~3, end), so each lane reads
+//    its quad with ONE aligned 16-byte load; the per-lane segment record {start & ~3 - 4 * first
+//    quad, end, tag, start} gives a quad's slots with one 16-byte smem load; loads are clamped
+//    into the list, so loads and hashes run unpredicated and one validity mask (start <= slot
+//    < end) is applied per quad;
 //  * filter position of w: word = top bits of x = w * K, bit = x & 31 (K odd, so x & 31 is a
 //    bijection of w & 31); one funnel rotate by (x - e) puts item e's bit at position e;
 //  * an item whose w misses the filter cannot be in N+(u) (the common case).  A lane with
@@ -473,13 +475,14 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                     if (S.prp[pi + 1] - S.prp[pi] >= 2) {
                         vs = rp_or[v];
                         vd = rp_or[v + 1] - vs;
-                        wt = (vd + kQuad - 1) / kQuad;
+                        // quads aligned to 16 bytes: [vs & ~3, vs + vd) in whole int4s
+                        wt = (vs + vd - (vs & ~3) + kQuad - 1) / kQuad;
                     }
                 }
                 const int incl = warp_incl_scan(wt, lane);
                 const int total = __shfl_sync(FULL, incl, 31);
                 const int pre = incl - wt;
-                S.seg[lane] = make_int4(vs - kQuad * pre, vs + vd, (s - A) | (pi << 8), 0);
+                S.seg[lane] = make_int4((vs & ~3) - kQuad * pre, vs + vd, (s - A) | (pi << 8), vs);
                 if (wt > 0) {  // the quad loop below reads N+(v)
                     prefetch_l2(col_or + vs);
                     if (((vs + vd - 1) >> 5) != (vs >> 5)) prefetch_l2(col_or + vs + vd - 1);
@@ -498,11 +501,11 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                     // lanes past the last quad belong to the last segment and get nval <= 0
                     const int jj = mine ? own : cur;
                     const int4 sg = S.seg[jj];
-                    const int sv0 = sg.x + kQuad * (k0 + lane);
-                    const int nval = sg.y - sv0;
-                    int w[kQuad];
-#pragma unroll
-                    for (int e = 0; e < kQuad; ++e) w[e] = __ldg(col_or + min(sv0 + e, sg.y - 1));
+                    const int sv0 = sg.x + kQuad * (k0 + lane);  // 16-byte aligned
+                    // one aligned 16-byte load per lane (clamped to the list's last quad)
+                    const int4 q4 = __ldg(reinterpret_cast<const int4*>(
+                        col_or + min(sv0, (sg.y - 1) & ~3)));
+                    const int w[kQuad] = {q4.x, q4.y, q4.z, q4.w};
                     unsigned cm = 0;
 #pragma unroll
                     for (int e = 0; e < kQuad; ++e) {
@@ -510,7 +513,9 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                         const unsigned word = S.filt[filter_word(x)];
                         cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
                     }
-                    cm &= (1u << min(max(nval, 0), kQuad)) - 1u;
+                    // valid entries: sg.w <= sv0 + e < sg.y
+                    cm &= ((1u << min(max(sg.y - sv0, 0), kQuad)) - 1u) &
+                          (0xfu << min(max(sg.w - sv0, 0), kQuad));
                     const unsigned hb = __ballot_sync(FULL, cm != 0u);
                     if (cm) S.rec[(rtail + __popc(hb & lt_mask)) & (kRec - 1)] =
                                 make_int2(sv0, (int)cm | (sg.z << 4));
