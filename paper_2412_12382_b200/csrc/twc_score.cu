@@ -425,7 +425,8 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                                                               const int* __restrict__ col_or,
                                                               int* __restrict__ t_or,
                                                               int* __restrict__ work,
-                                                              const int* __restrict__ range) {
+                                                              const int* __restrict__ range,
+                                                              const int2* __restrict__ vinfo) {
     extern __shared__ __align__(16) unsigned char k2_smem_raw[];
     K2WarpSmem* smem = reinterpret_cast<K2WarpSmem*>(k2_smem_raw);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -457,7 +458,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
             for (int i = lane; i < kGroupSlots / 4; i += 32) S.cnt[i] = 0u;
             __syncwarp();
             for (int i = lane; i < B - A; i += 32) {
-                const int x = col_or[A + i];
+                const int x = __ldcs(col_or + A + i);  // read once: staged, not kept in L1
                 S.list[i] = x;
                 const unsigned h = (unsigned)x * kFiltK;
                 atomicOr(&S.filt[filter_word(h)], 1u << (h & 31));
@@ -473,8 +474,9 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                     const int v = S.list[s - A];
                     pi = last_le(S.prp, np + 1, s);
                     if (S.prp[pi + 1] - S.prp[pi] >= 2) {
-                        vs = rp_or[v];
-                        vd = rp_or[v + 1] - vs;
+                        const int2 vi = vinfo[v];  // {rp_or[v], rp_or[v+1]}: one 8-byte load
+                        vs = vi.x;
+                        vd = vi.y - vs;
                         // quads aligned to 16 bytes: [vs & ~3, vs + vd) in whole int4s
                         wt = (vs + vd - (vs & ~3) + kQuad - 1) / kQuad;
                     }
@@ -973,7 +975,7 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         const int64_t warps = (int64_t)sms * occ * kK2Warps;
         const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(kPivotChunk, n / (8 * warps)));
         k2_intersect<<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or, w.t_or,
-                                                             w.work, range);
+                                                             w.work, range, w.vinfo);
         // hub pivots: found after K1, processed one per CTA (no work and an early exit when
         // the graph has none)
         k2_find_hubs<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, w.rp_or, w.hubs, w.nhubs,
