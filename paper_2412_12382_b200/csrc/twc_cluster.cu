@@ -65,11 +65,6 @@ __device__ __forceinline__ void uf_unite(int* parent, int u, int v) {
     }
 }
 
-__device__ __forceinline__ unsigned gcd_u(unsigned a, unsigned b) {
-    while (b) { unsigned t = a % b; a = b; b = t; }
-    return a;
-}
-
 __global__ void k_init_parent(int64_t n, int* __restrict__ parent) {
     int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u < n) parent[u] = (int)u;
@@ -196,13 +191,17 @@ __global__ void __launch_bounds__(256) k_hook_list(const int2* __restrict__ pair
                                                    int* __restrict__ parent) {
     const int beg = off[b], end = off[b + 1];
     const unsigned size = (unsigned)(end - beg);
-    // visit the band in a scrambled order (an affine bijection mod size) so that edges sharing
-    // a vertex are not handled by neighbouring threads at the same time
-    unsigned mult = 2654435761u % (size ? size : 1u);
-    while (size > 1 && (mult == 0 || gcd_u(mult, size) != 1u)) ++mult;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < size;
+    // visit the band in a scrambled order so that edges sharing a vertex (neighbours in the
+    // band, which keeps canonical row order) are not handled by neighbouring threads at the
+    // same time: j = (i * odd) mod 2^p is a bijection of [0, 2^p) (2^p >= size); the j >= size
+    // are skipped, so every edge of the band is visited exactly once
+    unsigned p2 = 1;
+    while (p2 < size) p2 <<= 1;
+    const unsigned mask = p2 - 1u;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < p2;
          i += gridDim.x * blockDim.x) {
-        const unsigned j = (unsigned)(((unsigned long long)i * mult) % size);
+        const unsigned j = (i * 2654435761u) & mask;
+        if (j >= size) continue;
         const int2 e = pairs[beg + j];
         uf_unite(parent, e.x, e.y);
     }
