@@ -573,7 +573,8 @@ constexpr int kHubFilterLog = 16;
 constexpr int kHubFilterWords = (1 << kHubFilterLog) / 32;
 
 struct K2HubWarp {
-    int pre[32], vst[32], vln[32], owner[32];
+    int4 seg[32];  // per lane: {start of N+(v) & ~3 - 4 * first quad, end, start, 0}
+    int owner[32];
     int ring[kHubRing];
 };
 struct K2HubSmem {
@@ -584,9 +585,8 @@ struct K2HubSmem {
     int hub;
 };
 
-__device__ __forceinline__ unsigned hub_hash(int w) {
-    return ((unsigned)w * 2654435761u) >> (32 - kHubFilterLog);
-}
+// filter position as K2's: word = top bits of x = w * K, bit = x & 31
+__device__ __forceinline__ unsigned hub_word(unsigned x) { return x >> (32 - kHubFilterLog + 5); }
 
 // hubs[] = pivots with more than kGroupSlots oriented neighbours (order irrelevant)
 __global__ void k2_find_hubs(int64_t n, const int* __restrict__ rp_or, int* __restrict__ hubs,
@@ -628,8 +628,8 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                 H.list[i] = x;
                 H.cnt[i] = 0;
             }
-            const unsigned hh = hub_hash(x);
-            atomicOr(&H.filt[hh >> 5], 1u << (hh & 31));
+            const unsigned hx = (unsigned)x * kFiltK;
+            atomicOr(&H.filt[hub_word(hx)], 1u << (hx & 31));
         }
         __syncthreads();
         for (int r0 = A + 32 * wid; r0 < B; r0 += 32 * kK2Warps) {
@@ -639,14 +639,12 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                 const int v = staged ? H.list[s - A] : col_or[s];
                 vs = rp_or[v];
                 vd = rp_or[v + 1] - vs;
-                wt = (vd + kQuad - 1) / kQuad;
+                wt = (vs + vd - (vs & ~3) + kQuad - 1) / kQuad;  // 16-byte aligned quads
             }
             const int incl = warp_incl_scan(wt, lane);
             const int total = __shfl_sync(FULL, incl, 31);
             const int pre = incl - wt;
-            W.pre[lane] = pre;
-            W.vst[lane] = vs;
-            W.vln[lane] = vd;
+            W.seg[lane] = make_int4((vs & ~3) - kQuad * pre, vs + vd, vs, 0);
             const unsigned nz = __ballot_sync(FULL, wt > 0);
             int cur = nz ? __ffs(nz) - 1 : 0;
             int head = 0, tail = 0;
@@ -657,23 +655,23 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                 const unsigned bits = __reduce_or_sync(FULL, starts ? (1u << (pre - k0)) : 0u);
                 __syncwarp();
                 const unsigned mine = bits & ((2u << lane) - 1u);
-                const int jj = mine ? W.owner[31 - __clz(mine)] : cur;
-                const int k = k0 + lane;
-                int i0 = 0;
+                const int own = W.owner[31 - __clz(mine | 1u)];
+                const int jj = mine ? own : cur;  // lanes past the end: jj's segment, masked
+                const int4 sg = W.seg[jj];
+                const int sv0 = sg.x + kQuad * (k0 + lane);  // 16-byte aligned
+                const int4 q4 = __ldg(reinterpret_cast<const int4*>(
+                    col_or + min(sv0, (sg.y - 1) & ~3)));
+                const int wq[kQuad] = {q4.x, q4.y, q4.z, q4.w};
                 unsigned cm = 0;
-                if (k < total) {
-                    i0 = (k - W.pre[jj]) * kQuad;
-                    const int sv0 = W.vst[jj] + i0;
-                    const int nval = min(kQuad, W.vln[jj] - i0);
 #pragma unroll
-                    for (int e = 0; e < kQuad; ++e) {
-                        if (e < nval) {
-                            const unsigned hh = hub_hash(col_or[sv0 + e]);
-                            if ((H.filt[hh >> 5] >> (hh & 31)) & 1u) cm |= 1u << e;
-                        }
-                    }
+                for (int e = 0; e < kQuad; ++e) {
+                    const unsigned x = (unsigned)wq[e] * kFiltK;
+                    const unsigned word = H.filt[hub_word(x)];
+                    cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
                 }
-                const int cbase = (jj << 16) | i0;
+                cm &= ((1u << min(max(sg.y - sv0, 0), kQuad)) - 1u) &
+                      (0xfu << min(max(sg.z - sv0, 0), kQuad));
+                const int cbase = (jj << 16) + (sv0 - sg.z);  // + e >= 0 for a valid entry
 #pragma unroll
                 for (int e = 0; e < kQuad; ++e) {
                     const bool c = (cm >> e) & 1u;
@@ -688,7 +686,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                     if (lane < cnt) {
                         const int e = W.ring[(head + lane) & (kHubRing - 1)];
                         const int j = e >> 16;
-                        const int sv = W.vst[j] + (e & 0xffff);  // slot of v -> w
+                        const int sv = W.seg[j].z + (e & 0xffff);  // slot of v -> w
                         const int w = col_or[sv];
                         const int* L = staged ? H.list : col_or + A;
                         const int q = staged ? lower_bound_bl(L, len, w) : lower_bound(L, len, w);
