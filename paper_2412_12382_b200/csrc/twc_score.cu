@@ -13,6 +13,7 @@
 // count arrays, which one int32 array plus atomics avoids on a GPU.  DESIGN.md Sec. 4.
 #include <algorithm>
 #include <climits>
+#include <vector>
 
 #include "twc_common.cuh"
 #include "twc_internal.h"
@@ -919,6 +920,33 @@ static int grid_for(int64_t items, int per_block, int max_blocks) {
     return (int)b;
 }
 
+// A per-thread, per-device side stream with a fork and a join event (created on first use and
+// kept for the life of the process); NULL if it cannot be created (then everything runs on the
+// caller's stream).
+struct AuxStream {
+    int dev = -1;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+static AuxStream* aux_stream() {
+    static thread_local std::vector<AuxStream> lanes;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    for (auto& x : lanes)
+        if (x.dev == dev) return &x;
+    AuxStream a;
+    a.dev = dev;
+    if (cudaStreamCreateWithFlags(&a.stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    lanes.push_back(a);
+    return &lanes.back();
+}
+
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
@@ -968,24 +996,34 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
             if (occ < 1) occ = 1;
         }
         record(ev, 1, s);
-        // pivots per queue grab: kPivotChunk, fewer when there are too few pivots to give every
-        // warp several grabs (small dense graphs), so the queue still balances the load
-        const int64_t warps = (int64_t)sms * occ * kK2Warps;
-        const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(kPivotChunk, n / (8 * warps)));
-        k2_intersect<<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or, w.t_or,
-                                                             w.work, range, w.vinfo);
-        // hub pivots: found after K1, processed one per CTA (no work and an early exit when
-        // the graph has none)
-        k2_find_hubs<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, w.rp_or, w.hubs, w.nhubs,
-                                                                range);
+        // hub pivots (|N+(u)| > kGroupSlots, one per CTA) run on a library-owned side stream,
+        // forked from and joined back to s: they start first (the largest tasks) and the
+        // persistent K2 grid fills the SM resources they leave, so neither kernel's tail idles
+        // the GPU.  No work and an early exit when the graph has no hub.
+        AuxStream* ax = aux_stream();
+        cudaStream_t sh = ax ? ax->stream : s;
+        if (ax) {
+            cudaEventRecord(ax->fork, s);
+            cudaStreamWaitEvent(sh, ax->fork, 0);
+        }
+        k2_find_hubs<<<(unsigned)((n + 255) / 256), 256, 0, sh>>>(n, w.rp_or, w.hubs, w.nhubs,
+                                                                 range);
         static int hub_set = 0;
         const size_t hsmem = sizeof(K2HubSmem);
         if (!hub_set) {
             cudaFuncSetAttribute(k2_hubs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
             hub_set = 1;
         }
-        k2_hubs<<<sms * 2, kK2Warps * 32, hsmem, s>>>(w.rp_or, w.col_or, w.hubs, w.nhubs,
-                                                       w.work + 1, w.t_or);
+        k2_hubs<<<sms * 2, kK2Warps * 32, hsmem, sh>>>(w.rp_or, w.col_or, w.hubs, w.nhubs,
+                                                        w.work + 1, w.t_or);
+        if (ax) cudaEventRecord(ax->join, sh);
+        // pivots per queue grab: kPivotChunk, fewer when there are too few pivots to give every
+        // warp several grabs (small dense graphs), so the queue still balances the load
+        const int64_t warps = (int64_t)sms * occ * kK2Warps;
+        const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(kPivotChunk, n / (8 * warps)));
+        k2_intersect<<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or, w.t_or,
+                                                             w.work, range, w.vinfo);
+        if (ax) cudaStreamWaitEvent(s, ax->join, 0);
         count_launches(3);
         record(ev, 2, s);
     }
