@@ -303,15 +303,14 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
 //    with a kFilterBits-bit hash filter of their entries (pivots with longer lists are hubs,
 //    left to K2h);
 //  * the group's slots are taken 32 at a time (one per lane, a "round"); slot u->v owns the
-//    items w in N+(v) if d+(u) >= 2, cut into quads of kQuad consecutive entries.  The quads of
-//    the 32 slots are flattened across the lanes (exclusive scan of the quad counts; the
-//    segment owning a quad is found with one __reduce_or_sync bit mask + one smem lookup), so
-//    each lane reads kQuad consecutive entries of one N+(v) and a warp reads a contiguous run.
-//    Quads are 16-byte aligned groups of col_or covering [start & ~3, end), so each lane reads
-//    its quad with ONE aligned 16-byte load; the per-lane segment record {start & ~3 - 4 * first
-//    quad, end, tag, start} gives a quad's slots with one 16-byte smem load; loads are clamped
-//    into the list, so loads and hashes run unpredicated and one validity mask (start <= slot
-//    < end) is applied per quad;
+//    items w in N+(v) if d+(u) >= 2, cut into groups of Q = kOct entries aligned to one 32-byte
+//    sector of col_or (covering [start & ~7, end)).  The groups of the 32 slots are flattened
+//    across the lanes (exclusive scan of the group counts; the segment owning a group is found
+//    with one __reduce_or_sync bit mask + one smem lookup), so each lane reads one aligned
+//    sector (two 16-byte loads) of one N+(v) and a warp reads a contiguous run.  The per-lane
+//    segment record {start & ~7 - 8 * first group, end, tag, start} gives a group's slots with
+//    one 16-byte smem load; loads are clamped into the list, so loads and hashes run
+//    unpredicated and one validity mask (start <= slot < end) is applied per group;
 //  * filter position of w: word = top bits of x = w * K, bit = x & 31 (K odd, so x & 31 is a
 //    bijection of w & 31); one funnel rotate by (x - e) puts item e's bit at position e;
 //  * an item whose w misses the filter cannot be in N+(u) (the common case).  A lane with
@@ -331,7 +330,8 @@ constexpr int kFilterLog = 13;
 constexpr int kFilterBits = 1 << kFilterLog;
 constexpr int kFilterWords = kFilterBits / 32;
 constexpr int kPivotChunk = 32;
-constexpr int kQuad = 4;
+constexpr int kQuad = 4;  // K2h: items per lane (one aligned 16-byte load)
+constexpr int kOct = 8;   // K2: items per lane (one aligned 32-byte sector, two 16-byte loads)
 constexpr int kRing = 128;  // candidate ring (an expansion stops before it would overflow)
 constexpr int kRec = 64;    // record ring, >= 31 + 32 pending records
 constexpr unsigned kFiltK = 2654435761u;
@@ -380,19 +380,20 @@ __device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int head, int
 // Expand records [rhead, rhead + cnt) (cnt <= 32, lane i takes record rhead + i) into the
 // candidate ring at tail while they fit; returns the number of records consumed (a prefix; at
 // least 24 when fewer than 32 candidates are pending).
+template <int Q>
 __device__ __forceinline__ int k2_expand(K2WarpSmem& S, int lane, int rhead, int cnt, int head,
                                          int& tail) {
     const int2 r = (lane < cnt) ? S.rec[(rhead + lane) & (kRec - 1)] : make_int2(0, 0);
-    const unsigned cm = (unsigned)r.y & 15u;
+    const unsigned cm = (unsigned)r.y & 0xffu;
     const int nc = __popc(cm);
     const int incl = warp_incl_scan(nc, lane);
     const bool fits = lane < cnt && incl <= kRing - (tail - head);
     const unsigned fb = __ballot_sync(FULL, fits);
     if (fits) {
         int pos = tail + incl - nc;
-        const int tag = r.y >> 4;
+        const int tag = r.y >> 8;
 #pragma unroll
-        for (int e = 0; e < kQuad; ++e) {
+        for (int e = 0; e < Q; ++e) {
             if ((cm >> e) & 1u) {
                 S.ring[pos & (kRing - 1)] = make_int2(r.x + e, tag);
                 ++pos;
@@ -406,11 +407,12 @@ __device__ __forceinline__ int k2_expand(K2WarpSmem& S, int lane, int rhead, int
 
 // Drain: expand pending records while at least `keep` remain and verify full warps of
 // candidates.
+template <int Q>
 __device__ __forceinline__ void k2_drain(K2WarpSmem& S, int lane, int keep, int A, int& rhead,
                                          int rtail, int& head, int& tail,
                                          const int* __restrict__ col_or, int* __restrict__ t_or) {
     while (rtail - rhead > keep) {
-        rhead += k2_expand(S, lane, rhead, min(32, rtail - rhead), head, tail);
+        rhead += k2_expand<Q>(S, lane, rhead, min(32, rtail - rhead), head, tail);
         __syncwarp();
         while (tail - head >= 32) {
             k2_verify(S, lane, head, 32, A, col_or, t_or);
@@ -421,6 +423,7 @@ __device__ __forceinline__ void k2_drain(K2WarpSmem& S, int lane, int keep, int 
 }
 
 // range: NULL (all pivots) or device {u_lo, u_hi} of a shard (the queue starts at u_lo)
+template <int Q>
 __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int chunk,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
@@ -478,14 +481,14 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                         const int2 vi = vinfo[v];  // {rp_or[v], rp_or[v+1]}: one 8-byte load
                         vs = vi.x;
                         vd = vi.y - vs;
-                        // quads aligned to 16 bytes: [vs & ~3, vs + vd) in whole int4s
-                        wt = (vs + vd - (vs & ~3) + kQuad - 1) / kQuad;
+                        // items in aligned groups of Q: [vs & ~(Q-1), vs + vd)
+                        wt = (vs + vd - (vs & ~(Q - 1)) + Q - 1) / Q;
                     }
                 }
                 const int incl = warp_incl_scan(wt, lane);
                 const int total = __shfl_sync(FULL, incl, 31);
                 const int pre = incl - wt;
-                S.seg[lane] = make_int4((vs & ~3) - kQuad * pre, vs + vd, (s - A) | (pi << 8), vs);
+                S.seg[lane] = make_int4((vs & ~(Q - 1)) - Q * pre, vs + vd, (s - A) | (pi << 8), vs);
                 if (wt > 0) {  // the quad loop below reads N+(v)
                     prefetch_l2(col_or + vs);
                     if (((vs + vd - 1) >> 5) != (vs >> 5)) prefetch_l2(col_or + vs + vd - 1);
@@ -504,32 +507,37 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                     // lanes past the last quad belong to the last segment and get nval <= 0
                     const int jj = mine ? own : cur;
                     const int4 sg = S.seg[jj];
-                    const int sv0 = sg.x + kQuad * (k0 + lane);  // 16-byte aligned
-                    // one aligned 16-byte load per lane (clamped to the list's last quad)
-                    const int4 q4 = __ldg(reinterpret_cast<const int4*>(
-                        col_or + min(sv0, (sg.y - 1) & ~3)));
-                    const int w[kQuad] = {q4.x, q4.y, q4.z, q4.w};
+                    const int sv0 = sg.x + Q * (k0 + lane);  // 4Q-byte aligned
+                    // Q / 4 aligned 16-byte loads per lane (clamped to the list's last group)
+                    const int4* src = reinterpret_cast<const int4*>(
+                        col_or + min(sv0, (sg.y - 1) & ~(Q - 1)));
+                    int w[Q];
+#pragma unroll
+                    for (int h = 0; h < Q / 4; ++h) {
+                        const int4 q4 = __ldg(src + h);
+                        w[4 * h] = q4.x; w[4 * h + 1] = q4.y; w[4 * h + 2] = q4.z; w[4 * h + 3] = q4.w;
+                    }
                     unsigned cm = 0;
 #pragma unroll
-                    for (int e = 0; e < kQuad; ++e) {
+                    for (int e = 0; e < Q; ++e) {
                         const unsigned x = (unsigned)w[e] * kFiltK;
                         const unsigned word = S.filt[filter_word(x)];
                         cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
                     }
                     // valid entries: sg.w <= sv0 + e < sg.y
-                    cm &= ((1u << min(max(sg.y - sv0, 0), kQuad)) - 1u) &
-                          (0xfu << min(max(sg.w - sv0, 0), kQuad));
+                    cm &= ((1u << min(max(sg.y - sv0, 0), Q)) - 1u) &
+                          (((1u << Q) - 1u) << min(max(sg.w - sv0, 0), Q));
                     const unsigned hb = __ballot_sync(FULL, cm != 0u);
                     if (cm) S.rec[(rtail + __popc(hb & lt_mask)) & (kRec - 1)] =
-                                make_int2(sv0, (int)cm | (sg.z << 4));
+                                make_int2(sv0, (int)cm | (sg.z << 8));
                     rtail += __popc(hb);
                     cur = __shfl_sync(FULL, jj, 31);
                     __syncwarp();
-                    k2_drain(S, lane, 31, A, rhead, rtail, head, tail, col_or, t_or);
+                    k2_drain<Q>(S, lane, 31, A, rhead, rtail, head, tail, col_or, t_or);
                 }
                 __syncwarp();  // seg / owner are rewritten by the next round
             }
-            k2_drain(S, lane, 0, A, rhead, rtail, head, tail, col_or, t_or);
+            k2_drain<Q>(S, lane, 0, A, rhead, rtail, head, tail, col_or, t_or);
             if (tail > head) k2_verify(S, lane, head, tail - head, A, col_or, t_or);
             __syncwarp();
             for (int i = lane; i < B - A; i += 32) {
@@ -990,9 +998,10 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         const size_t smem = kK2Warps * sizeof(K2WarpSmem);
         static int occ = 0;
         if (occ == 0) {
-            cudaFuncSetAttribute(k2_intersect, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(k2_intersect<kOct>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_intersect, kK2Warps * 32, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_intersect<kOct>, kK2Warps * 32,
+                                                          smem);
             if (occ < 1) occ = 1;
         }
         record(ev, 1, s);
@@ -1021,8 +1030,8 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         // warp several grabs (small dense graphs), so the queue still balances the load
         const int64_t warps = (int64_t)sms * occ * kK2Warps;
         const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(kPivotChunk, n / (8 * warps)));
-        k2_intersect<<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or, w.t_or,
-                                                             w.work, range, w.vinfo);
+        k2_intersect<kOct><<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or,
+                                                                   w.t_or, w.work, range, w.vinfo);
         if (ax) cudaStreamWaitEvent(s, ax->join, 0);
         count_launches(3);
         record(ev, 2, s);
