@@ -94,7 +94,10 @@ def launch_summary(tag, path):
     # the last complete fused step (twc_score_sweep: contains k_band_place)
     steps = [seq[a:b] for a, b in zip(idx[:-1], idx[1:])]
     fused = [st for st in steps if any("k_band_place" in nm for nm, _ in st)]
-    chosen = fused[-1] if fused else steps[-1]
+    # complete = as many sweep steps as any fused step (the capture limit can cut the last one)
+    nfin = [sum("k_finalize" in nm for nm, _ in st) for st in fused]
+    full = [st for st, c in zip(fused, nfin) if nfin and c == max(nfin)]
+    chosen = full[-1] if full else steps[-1]
     # a fused step ends at its last k_finalize (the separate calls may follow in the same chunk)
     last_fin = max((k for k, (nm, _) in enumerate(chosen) if "k_finalize" in nm), default=len(chosen) - 1)
     last = [x for x in chosen[:last_fin + 1] if not x[0].startswith("at::")]
