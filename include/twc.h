@@ -24,7 +24,12 @@
  *  Streams. `stream` is a cudaStream_t (NULL = legacy default stream).  Device calls only
  *           enqueue work on it and return without synchronising (outputs are valid once the
  *           stream reaches them), except twc_validate_csr and the *_host calls, which
- *           synchronise the stream before returning.
+ *           synchronise the stream before returning.  The scoring calls may fork part of
+ *           their work (the hub-pivot intersection) onto a library-owned side stream of the
+ *           calling thread and join it back to `stream` with events before they return, so
+ *           stream order, event timing and CUDA-graph capture of `stream` see one call as one
+ *           unit; the *_host_async calls copy results back on a library-owned copy stream the
+ *           same way.
  *  Errors.  Calls return a twc_status.  TWC_EINVAL: a null pointer where data is required
  *           (n > 0 or m > 0), n or m out of range, rowptr_bytes not in {4, 8}, NaN delta,
  *           k < 1.  TWC_EWORKSPACE: workspace too small or misaligned.  TWC_ECUDA: a CUDA launch
