@@ -10,11 +10,13 @@
 // sum over b of |N+(b)| membership tests against N+(a) plus, per triangle, |N+(c)| tests
 // against C: O(m * alpha^2) as Table 1 states.
 //
-// k4_pivots<false>: one warp per pivot with |N+(a)| <= kK4Cap; N+(a), its per-slot counters and
-//   the current C (ids, slot in N+(a), slot in N+(b)) live in the warp's shared memory; every
-//   membership test is a binary search in shared memory; counters of N+(a) are flushed once.
-// k4_pivots<true>:  the few pivots with longer lists, N+(a) read from global memory and C kept
-//   in a per-warp global scratch (|C| <= |N+(b)| <= sqrt(2m) under the degree orientation).
+// k4_masks<W>: pivots with |N+(a)| <= 64 W (W = 1, 2, 4): the 4-cliques of pivot a are the
+//   triangles of the graph G_a induced on N+(a); its edges are found by K2's flattened item
+//   scan (filter + search in the staged N+(a)) and kept as W-word neighbour masks, so the
+//   count of every edge is a popcount of two masks (see the kernel).
+// k4_pivot<true> / k4_big: the few pivots with longer lists, N+(a) read from global memory and
+//   C = N+(a) & N+(b) kept in a per-warp global scratch (|C| <= |N+(b)| <= sqrt(2m) under the
+//   degree orientation), each c in C probed against N+(c).
 // The counts are accumulated in oriented-slot order (64-bit) and gathered to canonical order by
 // the score epilogue (K3) together with t, wedge and TW.
 #include <algorithm>
@@ -123,27 +125,212 @@ __device__ __forceinline__ void k4_pivot(int a, int lane, const int* __restrict_
     }
 }
 
-// Small pivots (3 <= |N+(a)| <= kK4Cap): warps take chunks of consecutive pivots.
-__global__ void __launch_bounds__(kK4Warps * 32) k4_small(int64_t n, int chunk,
-                                                          const int* __restrict__ rp_or,
-                                                          const int* __restrict__ col_or,
-                                                          unsigned long long* __restrict__ k4_or,
-                                                          int* __restrict__ work) {
-    __shared__ K4WarpSmem smem[kK4Warps];
+// ---- pivots with 3 <= |N+(a)| <= 64: the 4-cliques whose lowest vertex is a are the triangles
+// of the graph G_a induced on N+(a).  One warp per pivot, N+(a) staged in shared memory with a
+// 2,048-bit filter; the items (x in N+(a), y in N+(x)) are flattened across the lanes (segment
+// owner lookup) and y is searched in N+(a) only when the filter hits.  Pass 1 finds every edge
+// {x, y} of G_a and records it in 64-bit neighbour masks nbr[]; pass 2 finds the same edges
+// again and, for each, k = popc(nbr[x] & nbr[y]) = the triangles of G_a on it = the 4-cliques
+// {a, x, y, z} on edge (x, y) counted from pivot a, added to (x, y)'s oriented slot; the pivot
+// edges (a, x) get half the sum of k over the edges of G_a at x.  (Each 4-clique is counted from
+// its lowest vertex only, as in k4_pivot.)
+// W = 1 with pivots GROUPED like K2: consecutive pivots whose lists total <= 64 slots share one
+// staged list, filter and mask array (bits are only ever set between two entries of the same
+// pivot, so a mask popcount still counts within one G_a), which amortises the per-pivot setup
+// over ~7 pivots on config 5.  prp[] holds the group's pivot offsets; a slot's pivot is found by
+// a short search in it.
+constexpr int kK4Edges = 128;
+
+// W 64-bit words per neighbour mask: up to 64 W slots staged, a 2,048 W-bit filter
+template <int W>
+struct K4GroupSmem {
+    int list[64 * W];
+    unsigned filt[64 * W];
+    unsigned long long nbr[64 * W * W];  // nbr[i * W + w]
+    int acc[64 * W];
+    int prp[33];
+    int4 seg[32];
+    int owner[32];
+    int2 edge[kK4Edges];  // edges of the G_a found by pass 1: {slot of x -> y, ix | iy << 10}
+    int nedge;
+};
+
+template <int W>
+__device__ __forceinline__ unsigned k4_filt_word(unsigned h) {
+    return h >> (W == 1 ? 26 : W == 2 ? 25 : 24);  // 64 W words
+}
+
+template <int W, int PASS>
+__device__ __forceinline__ void k4_group_pass(K4GroupSmem<W>& S, int lane, int len, int np,
+                                              const int* __restrict__ rp_or,
+                                              const int* __restrict__ col_or,
+                                              unsigned long long* __restrict__ k4_or) {
+    for (int r0 = 0; r0 < len; r0 += 32) {  // rounds of 32 slots of the group
+        const int ix = r0 + lane;
+        int wt = 0, xs = 0, xe = 0, plo = 0, phi = 0;
+        if (ix < len) {
+            const int pi = last_le(S.prp, np + 1, ix);
+            plo = S.prp[pi];
+            phi = S.prp[pi + 1];
+            if (phi - plo >= 3) {  // a pivot with < 3 oriented neighbours has no 4-clique
+                const int x = S.list[ix];
+                xs = rp_or[x];
+                xe = rp_or[x + 1];
+                wt = (xe - (xs & ~7) + 7) >> 3;  // aligned 8-entry sectors covering [xs, xe)
+            }
+        }
+        const int incl = warp_incl_scan(wt, lane);
+        const int total = __shfl_sync(FULL, incl, 31);
+        const int pre = incl - wt;
+        // {first sector - 8 * first item, end, start, the pivot's slots [plo, phi) in the group}
+        S.seg[lane] = make_int4((xs & ~7) - 8 * pre, xe, xs, plo | (phi << 10));
+        const unsigned nz = __ballot_sync(FULL, wt > 0);
+        int cur = nz ? __ffs(nz) - 1 : 0;
+        __syncwarp();
+        for (int k0 = 0; k0 < total; k0 += 32) {
+            const bool starts = wt > 0 && pre >= k0 && pre < k0 + 32;
+            if (starts) S.owner[pre - k0] = lane;
+            const unsigned bits = __reduce_or_sync(FULL, starts ? (1u << (pre - k0)) : 0u);
+            __syncwarp();
+            const unsigned mine = bits & ((2u << lane) - 1u);
+            const int own = S.owner[31 - __clz(mine | 1u)];
+            const int jj = mine ? own : cur;
+            const int4 sg = S.seg[jj];
+            const int sv0 = sg.x + 8 * (k0 + lane);  // 32-byte aligned
+            const int4* src = reinterpret_cast<const int4*>(col_or + min(sv0, (sg.y - 1) & ~7));
+            const int4 qa = __ldg(src), qb = __ldg(src + 1);
+            const int y[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+            unsigned cm = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const unsigned h = (unsigned)y[e] * 2654435761u;
+                const unsigned word = S.filt[k4_filt_word<W>(h)];
+                cm |= __funnelshift_r(word, word, h - (unsigned)e) & (1u << e);
+            }
+            cm &= ((1u << min(max(sg.y - sv0, 0), 8)) - 1u) &
+                  (0xffu << min(max(sg.z - sv0, 0), 8));
+            const int lo = sg.w & 1023, hi = sg.w >> 10, ixx = r0 + jj;
+            while (cm) {  // filter hits (rare): search the pivot's staged list
+                const int e = __ffs(cm) - 1;
+                cm &= cm - 1u;
+                const int q = find_sorted(S.list + lo, hi - lo, y[e]);
+                if (q >= 0) {  // edge {x, y} of G_a
+                    const int iy = lo + q;
+                    if (PASS == 1) {
+                        atomicOr(&S.nbr[ixx * W + (iy >> 6)], 1ull << (iy & 63));
+                        atomicOr(&S.nbr[iy * W + (ixx >> 6)], 1ull << (ixx & 63));
+                        const int pos = atomicAdd(&S.nedge, 1);  // kept for the counting step
+                        if (pos < kK4Edges) S.edge[pos] = make_int2(sv0 + e, ixx | (iy << 10));
+                    } else {
+                        int k = 0;
+#pragma unroll
+                        for (int q = 0; q < W; ++q) k += __popcll(S.nbr[ixx * W + q] & S.nbr[iy * W + q]);
+                        if (k) {
+                            atomicAdd(&k4_or[sv0 + e], (unsigned long long)k);  // (x, y)
+                            atomicAdd(&S.acc[ixx], k);
+                            atomicAdd(&S.acc[iy], k);
+                        }
+                    }
+                }
+            }
+            cur = __shfl_sync(FULL, jj, 31);
+            __syncwarp();
+        }
+        __syncwarp();
+    }
+}
+
+// W = 1: groups of consecutive pivots with |N+(a)| <= 64 (<= 64 slots per group); W = 2, 4: one
+// pivot with 32 W < |N+(a)| <= 64 W per group.
+template <int W>
+__global__ void __launch_bounds__(kK4Warps * 32) k4_groups(int64_t n, int chunk,
+                                                           const int* __restrict__ rp_or,
+                                                           const int* __restrict__ col_or,
+                                                           unsigned long long* __restrict__ k4_or,
+                                                           int* __restrict__ work) {
+    extern __shared__ __align__(16) unsigned char k4g_smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    K4WarpSmem& S = smem[wid];
+    K4GroupSmem<W>& S = reinterpret_cast<K4GroupSmem<W>*>(k4g_smem_raw)[wid];
     for (;;) {
         int base = 0;
         if (lane == 0) base = atomicAdd(work, chunk);
         base = __shfl_sync(FULL, base, 0);
         if (base >= n) break;
-        const int end = (int)min((int64_t)base + chunk, n);
-        for (int a = base; a < end; ++a) {
-            const int da = rp_or[a + 1] - rp_or[a];
-            if (da < 3 || da > kK4Cap) continue;  // no 4-clique / a big pivot
-            k4_pivot<false>(a, lane, rp_or, col_or, k4_or, S.list, S.cnt, S.cid, S.cpa, S.cpb);
+        const int gend = (int)min((int64_t)base + chunk, n);
+        int u = base;
+        while (u < gend) {
+            const int np_max = W == 1 ? min(32, gend - u) : 1;
+            const int A = rp_or[u];
+            const int e_l = (lane < np_max) ? rp_or[u + lane + 1] : INT_MAX;
+            const unsigned fit = __ballot_sync(
+                FULL, lane < np_max && e_l - A <= 64 * W && (W == 1 || e_l - A > 32 * W));
+            if (fit == 0u) {  // another size class (or k4_big)
+                ++u;
+                continue;
+            }
+            const int np = __popc(fit);
+            const int B = __shfl_sync(FULL, e_l, np - 1), len = B - A;
+            if (lane == 0) S.prp[0] = 0;
+            if (lane < np) S.prp[lane + 1] = e_l - A;
+            for (int i = lane; i < 64 * W; i += 32) {
+                S.filt[i] = 0u;
+                S.acc[i] = 0;
+            }
+            for (int i = lane; i < len * W; i += 32) S.nbr[i] = 0ull;
+            __syncwarp();
+            for (int i = lane; i < len; i += 32) {
+                const int x = col_or[A + i];
+                S.list[i] = x;
+                const unsigned h = (unsigned)x * 2654435761u;
+                atomicOr(&S.filt[k4_filt_word<W>(h)], 1u << (h & 31));
+            }
+            __syncwarp();
+            if (lane == 0) S.nedge = 0;
+            __syncwarp();
+            k4_group_pass<W, 1>(S, lane, len, np, rp_or, col_or, k4_or);
+            __syncwarp();
+            const int ne = S.nedge;
+            if (ne <= kK4Edges) {  // count from the kept edge list
+                for (int i = lane; i < ne; i += 32) {
+                    const int2 ed = S.edge[i];
+                    const int ixx = ed.y & 1023, iy = ed.y >> 10;
+                    int k = 0;
+#pragma unroll
+                    for (int q = 0; q < W; ++q) k += __popcll(S.nbr[ixx * W + q] & S.nbr[iy * W + q]);
+                    if (k) {
+                        atomicAdd(&k4_or[ed.x], (unsigned long long)k);  // (x, y)
+                        atomicAdd(&S.acc[ixx], k);
+                        atomicAdd(&S.acc[iy], k);
+                    }
+                }
+            } else {  // too many edges to keep: find them again
+                k4_group_pass<W, 2>(S, lane, len, np, rp_or, col_or, k4_or);
+            }
+            __syncwarp();
+            for (int i = lane; i < len; i += 32) {
+                const int c = S.acc[i];
+                if (c) atomicAdd(&k4_or[A + i], (unsigned long long)(c / 2));  // (a, x)
+            }
+            __syncwarp();
+            u += np;
         }
     }
+}
+
+template <int W>
+static void launch_k4_groups(int64_t n, const int* rp_or, const int* col_or,
+                             unsigned long long* k4_or, int* work, cudaStream_t s) {
+    const size_t smem = kK4Warps * sizeof(K4GroupSmem<W>);
+    static int occ = 0;
+    if (occ == 0) {
+        cudaFuncSetAttribute(k4_groups<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_groups<W>, kK4Warps * 32, smem);
+        if (occ < 1) occ = 1;
+    }
+    const int sms = num_sms();
+    const int64_t warps = (int64_t)sms * occ * kK4Warps;
+    const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(32, n / (8 * warps)));
+    k4_groups<W><<<sms * occ, kK4Warps * 32, smem, s>>>(n, chunk, rp_or, col_or, k4_or, work);
 }
 
 // big[] = pivots with more than kK4Cap oriented neighbours
@@ -187,7 +374,7 @@ size_t k4_ws_bytes(int64_t n, int64_t m) {
     Carver cv(nullptr, 0);
     cv.take<unsigned long long>(m);  // k4_or
     cv.take<int>(n);                 // big pivots
-    cv.take<int>(4);                 // counters
+    cv.take<int>(5);                 // counters
     const int64_t cmax = (int64_t)std::sqrt(2.0 * (double)m) + 2;
     cv.take<int>((size_t)k4_big_warps() * 3 * cmax);
     return cv.used;
@@ -200,27 +387,20 @@ cudaError_t k4_count(int64_t n, int64_t m, const int* rp_or, const int* col_or, 
     Carver cv(ws, ws_bytes);
     unsigned long long* k4_or = cv.take<unsigned long long>(m);
     int* big = cv.take<int>(n);
-    int* ctr = cv.take<int>(4);  // [0] small queue, [1] big count, [2] big queue
+    int* ctr = cv.take<int>(5);  // [0] masks W=1, [1] big count, [2] big queue, [3] W=2, [4] W=4
     const int64_t cmax = (int64_t)std::sqrt(2.0 * (double)m) + 2;
     int* scratch = cv.take<int>((size_t)k4_big_warps() * 3 * cmax);
     *k4_or_out = k4_or;
     cudaMemsetAsync(k4_or, 0, sizeof(unsigned long long) * (size_t)m, s);
-    cudaMemsetAsync(ctr, 0, 4 * sizeof(int), s);
-    const int sms = num_sms();
-    // one resident wave: the warps are latency-bound (a global round trip per slot and per
-    // triangle), so occupancy is what hides the latency
-    static int occ = 0;
-    if (occ == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_small, kK4Warps * 32, 0);
-        if (occ < 1) occ = 1;
-    }
-    const int64_t warps = (int64_t)sms * occ * kK4Warps;
-    const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(16, n / (8 * warps)));
-    k4_small<<<sms * occ, kK4Warps * 32, 0, s>>>(n, chunk, rp_or, col_or, k4_or, ctr);
+    cudaMemsetAsync(ctr, 0, 5 * sizeof(int), s);
+    // pivots with |N+(a)| <= 256 by size class (mask words W = 1, 2, 4); longer lists below
+    launch_k4_groups<1>(n, rp_or, col_or, k4_or, ctr + 0, s);
+    launch_k4_groups<2>(n, rp_or, col_or, k4_or, ctr + 3, s);
+    launch_k4_groups<4>(n, rp_or, col_or, k4_or, ctr + 4, s);
     k4_find_big<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rp_or, big, ctr + 1);
     k4_big<<<k4_big_warps() / 4, 128, 0, s>>>(big, ctr + 1, rp_or, col_or, k4_or, scratch,
                                                (int)cmax, ctr + 2);
-    count_launches(3);
+    count_launches(5);
     return cudaGetLastError();
 }
 
