@@ -38,6 +38,10 @@ METRICS = [
     ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier"),
     ("smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio", "stall math"),
     ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall wait"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "global load sectors"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "global load requests"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", "global RED requests"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum", "global atomic requests"),
 ]
 
 
@@ -64,8 +68,15 @@ def full_summary(tag, rep):
         lines.append("| metric | value |")
         lines.append("|---|---|")
         for key, label in METRICS:
-            if key in col:
-                lines.append(f"| {label} (`{key}`) | {r[col[key]]} {units[col[key]]} |")
+            ck = key if key in col else next((h for h in col if h.endswith("." + key)), None)
+            if ck is not None:
+                lines.append(f"| {label} (`{key}`) | {r[col[ck]]} {units[col[ck]]} |")
+        try:  # derived: sectors per global load request
+            sec = float(r[col["l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"]].replace(",", ""))
+            req = float(r[col["l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"]].replace(",", ""))
+            lines.append(f"| sectors per global load request | {sec / req:.2f} |")
+        except (KeyError, ValueError, ZeroDivisionError):
+            pass
         lines.append("")
         if "k2_intersect" in name and k2 is None:
             rd = to_bytes(r[col["dram__bytes_read.sum"]], units[col["dram__bytes_read.sum"]])
