@@ -23,7 +23,7 @@ METRICS = [
     ("gpu__time_duration.sum", "duration"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % peak"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % peak"),
     ("lts__t_bytes.sum", "L2 bytes"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
