@@ -166,38 +166,68 @@ __global__ void __launch_bounds__(kSlotThreads, 8) k1_bits(
     }
 }
 
-// Exclusive scans of the two per-tile count arrays (one block; ntiles ~ 2m / 2048).
+// Exclusive scans of the two per-tile count arrays (one block; ntiles ~ 2m / 2048).  Both
+// counts travel packed in one 64-bit value (out << 32 | upper; each total <= m < 2^32, so the
+// low half never carries).  Warp w owns one contiguous segment: a coalesced sum pass (four
+// 32-tile chunks in flight), one scan of the 32 segment sums, then a warp-scan rewrite of the
+// segment -- no block barrier per 1,024 tiles (config 5, 34k tiles: 39 -> 28 us in the ncu launch list).
+__device__ __forceinline__ unsigned long long tile_pack(const int* a, const int* b, int64_t i) {
+    return ((unsigned long long)(unsigned)a[i] << 32) | (unsigned)b[i];
+}
+
 __global__ void __launch_bounds__(1024) k1_tile_scan(int64_t ntiles, int* __restrict__ a,
                                                      int* __restrict__ b) {
-    __shared__ int s_wa[32], s_wb[32];
-    __shared__ int s_ca, s_cb;
+    __shared__ unsigned long long s_w[32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (threadIdx.x == 0) { s_ca = 0; s_cb = 0; }
+    const int64_t seg = (ntiles + 31) / 32;
+    const int64_t lo = min(ntiles, (int64_t)wid * seg), hi = min(ntiles, lo + seg);
+    unsigned long long part = 0;
+    for (int64_t base = lo; base < hi; base += 128) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t i = base + 32 * k + lane;
+            if (i < hi) part += tile_pack(a, b, i);
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(FULL, part, d);
+    if (lane == 0) s_w[wid] = part;
     __syncthreads();
-    for (int64_t base = 0; base < ntiles; base += 1024) {
-        const int64_t i = base + threadIdx.x;
-        const int va = i < ntiles ? a[i] : 0, vb = i < ntiles ? b[i] : 0;
-        const int ia = warp_incl_scan(va, lane), ib = warp_incl_scan(vb, lane);
-        if (lane == 31) { s_wa[wid] = ia; s_wb[wid] = ib; }
-        __syncthreads();
-        if (wid == 0) {
-            const int xa = s_wa[lane], xb = s_wb[lane];
-            const int ya = warp_incl_scan(xa, lane), yb = warp_incl_scan(xb, lane);
-            s_wa[lane] = ya - xa;
-            s_wb[lane] = yb - xb;
+    if (wid == 0) {
+        const unsigned long long x = s_w[lane];
+        unsigned long long y = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long z = __shfl_up_sync(FULL, y, d);
+            if (lane >= d) y += z;
         }
-        __syncthreads();
-        const int ca = s_ca, cb = s_cb;
-        if (i < ntiles) {
-            a[i] = ca + s_wa[wid] + ia - va;
-            b[i] = cb + s_wb[wid] + ib - vb;
+        s_w[lane] = y - x;
+    }
+    __syncthreads();
+    unsigned long long run = s_w[wid];
+    for (int64_t base = lo; base < hi; base += 128) {
+        unsigned long long v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t i = base + 32 * k + lane;
+            v[k] = i < hi ? tile_pack(a, b, i) : 0ull;
         }
-        __syncthreads();
-        if (threadIdx.x == 1023) {
-            s_ca = ca + s_wa[wid] + ia;
-            s_cb = cb + s_wb[wid] + ib;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            unsigned long long incl = v[k];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned long long z = __shfl_up_sync(FULL, incl, d);
+                if (lane >= d) incl += z;
+            }
+            const int64_t i = base + 32 * k + lane;
+            const unsigned long long ex = run + incl - v[k];
+            if (i < hi) {
+                a[i] = (int)(ex >> 32);
+                b[i] = (int)(ex & 0xffffffffull);
+            }
+            run += __shfl_sync(FULL, incl, 31);
         }
-        __syncthreads();
     }
 }
 
