@@ -421,7 +421,14 @@ def main_b200(args):
     roofline = {"bound": "hbm", "kernel": "k2_intersect", "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": k2_bytes, "peak_source": peak_src,
-                "k2_ms_avg": 1000 * k2_avg_s}
+                "k2_ms_avg": 1000 * k2_avg_s,
+                "frac_of_8000": achieved / 8000.0}
+    if traffic:
+        # SURVEY 8(d) figure 1: measured DRAM bytes per launch (committed ncu capture) over the
+        # live K2 time, against the measured copy peak and north_star's ~8 TB/s
+        dram_gbs = traffic / k2_avg_s / 1e9
+        roofline["dram"] = {"achieved": dram_gbs, "unit": "GB/s", "frac": dram_gbs / peak,
+                            "frac_of_8000": dram_gbs / 8000.0}
     if k2prof and k2prof.get("warp_inst_per_launch"):
         # K2 is bound by instruction issue and load latency, not by DRAM:
         # its warp instructions per launch (committed ncu capture) over the live K2 time,
