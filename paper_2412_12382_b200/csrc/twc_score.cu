@@ -551,7 +551,11 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
 #pragma unroll
                     for (int e = 0; e < Q; ++e) {
                         const unsigned x = (unsigned)w[e] * kFiltK;
-                        const unsigned word = S.filt[filter_word(x)];
+                        // opaque word index: keeps ptxas from folding the shift into
+                        // (x >> 22) & 0x3fc + base (3 ops) so the address is SHF + LEA
+                        unsigned fw = filter_word(x);
+                        asm("" : "+r"(fw));
+                        const unsigned word = S.filt[fw];
                         cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
                     }
                     // valid entries: sg.w <= sv0 + e < sg.y
