@@ -25,6 +25,9 @@ METRICS = [
     ("dram__bytes_write.sum", "DRAM write"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % peak"),
     ("lts__t_bytes.sum", "L2 bytes"),
+    ("lts__t_sectors.sum", "L2 sectors (x 32 B = L2 bytes)"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 % peak"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
