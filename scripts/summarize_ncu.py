@@ -28,6 +28,10 @@ METRICS = [
     ("lts__t_sectors.sum", "L2 sectors (x 32 B = L2 bytes)"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 % peak"),
     ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1 data pipe (LSU wavefronts) % peak"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smem load bank conflicts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum", "smem atomic bank conflicts"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
