@@ -349,9 +349,10 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
 //    verified 32 at a time by binary search in the staged sorted N+(u), so the prefix work and
 //    the search run on full warps.  Record and candidate entries are self-contained, so the
 //    rings carry over between the rounds of a group and drain only when full or at its end;
-//  * a verified hit adds 1 to t(u,w) and t(u,v) in per-warp byte counters (a count found from
-//    one pivot is at most |N+(u)| - 1 <= 255; flushed once per group) and 1 to t(v,w) with one
-//    global reduction;
+//  * a verified hit adds 1 to t(u,w) in a per-warp byte counter (a count found from one pivot
+//    is at most |N+(u)| - 1 <= 255; flushed once per group) and 1 to t(u,v) and t(v,w) with
+//    global reductions (t(u,v) moved off shared memory: K2 is bound by the L1/shared data
+//    pipe, and a verify batch's t(u,v) hits pile onto a few words -- bank-conflict replays);
 //  * the round setup prefetches each lane's N+(v) into L2, so the quad loop's loads find it.
 // DESIGN.md Sec. 4.1 lists the variants measured on the way (ncu evidence per step).
 constexpr int kK2Warps = 8;
@@ -401,7 +402,7 @@ __device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int head, int
         if (q < len && L[q] == w) {
             const int i = plo + q;
             atomicAdd(&S.cnt[i >> 2], 1u << (8 * (i & 3)));    // t(u, w)
-            atomicAdd(&S.cnt[so >> 2], 1u << (8 * (so & 3)));  // t(u, v)
+            atomicAdd(&t_or[A + so], 1);                      // t(u, v)
             atomicAdd(&t_or[sv], 1);                          // t(v, w)
         }
     }
