@@ -349,10 +349,10 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
 //    verified 32 at a time by binary search in the staged sorted N+(u), so the prefix work and
 //    the search run on full warps.  Record and candidate entries are self-contained, so the
 //    rings carry over between the rounds of a group and drain only when full or at its end;
-//  * a verified hit adds 1 to t(u,w) in a per-warp byte counter (a count found from one pivot
-//    is at most |N+(u)| - 1 <= 255; flushed once per group) and 1 to t(u,v) and t(v,w) with
-//    global reductions (t(u,v) moved off shared memory: K2 is bound by the L1/shared data
-//    pipe, and a verify batch's t(u,v) hits pile onto a few words -- bank-conflict replays);
+//  * a verified hit adds 1 to t(u,w), t(u,v) and t(v,w) with three global reductions (the
+//    first two land in the group's own slot range [A, B), a few sectors per verify batch).
+//    Per-warp shared byte counters were used before; K2 is bound by the L1/shared data pipe,
+//    and their atomics cost bank-conflict replays plus a flush per group;
 //  * the round setup prefetches each lane's N+(v) into L2, so the quad loop's loads find it.
 // DESIGN.md Sec. 4.1 lists the variants measured on the way (ncu evidence per step).
 constexpr int kK2Warps = 8;
@@ -367,11 +367,10 @@ constexpr int kRing = 128;  // candidate ring (an expansion stops before it woul
 constexpr int kRec = 64;    // record ring, >= 31 + 32 pending records
 constexpr unsigned kFiltK = 2654435761u;
 
-// 4,612 bytes per warp: 5 CTAs of 8 warps fit the 196 KB smem carveout and leave 60 KB of L1
+// 4,368 bytes per warp: 5 CTAs of 8 warps fit the 196 KB smem carveout and leave 60 KB of L1
 // for the N+(v) reads (a 228 KB carveout, i.e. 28 KB of L1, made the same kernel 18 % slower).
 struct K2WarpSmem {
     int list[kGroupSlots];          // staged col_or[A, B)
-    unsigned cnt[kGroupSlots / 4];  // byte counters t(u,v)/t(u,w) for slots [A, B)
     unsigned filt[kFilterWords];
     int prp[33];                    // group pivot offsets rp_or[u0 .. u0+np]
     int owner[32];                  // quad-segment owner lookup
@@ -401,7 +400,7 @@ __device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int head, int
         const int q = lower_bound_bl(L, len, w);
         if (q < len && L[q] == w) {
             const int i = plo + q;
-            atomicAdd(&S.cnt[i >> 2], 1u << (8 * (i & 3)));    // t(u, w)
+            atomicAdd(&t_or[A + i], 1);                       // t(u, w)
             atomicAdd(&t_or[A + so], 1);                      // t(u, v)
             atomicAdd(&t_or[sv], 1);                          // t(v, w)
         }
@@ -490,7 +489,6 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
             if (lane == 0) S.prp[0] = A;
             if (lane < np) S.prp[lane + 1] = e_l;
             for (int i = lane; i < kFilterWords; i += 32) S.filt[i] = 0u;
-            for (int i = lane; i < kGroupSlots / 4; i += 32) S.cnt[i] = 0u;
             __syncwarp();
             for (int i = lane; i < B - A; i += 32) {
                 const int x = __ldcs(col_or + A + i);  // read once: staged, not kept in L1
@@ -574,11 +572,6 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
             }
             k2_drain<Q>(S, lane, 0, A, rhead, rtail, head, tail, col_or, t_or);
             if (tail > head) k2_verify(S, lane, head, tail - head, A, col_or, t_or);
-            __syncwarp();
-            for (int i = lane; i < B - A; i += 32) {
-                const unsigned c = (S.cnt[i >> 2] >> (8 * (i & 3))) & 0xffu;
-                if (c) atomicAdd(&t_or[A + i], (int)c);
-            }
             __syncwarp();
             u += np;
         }
