@@ -56,6 +56,16 @@ def parse():
     return ap.parse_args()
 
 
+def config_dict(cfg, g, deltas, world):
+    """The `config` object of the JSON line; identical for both arms (--impl b200|reference)."""
+    return {"workload": workload_desc(cfg, g, len(deltas)), "n": g.n, "m": g.m,
+            "thresholds": list(deltas), "rowptr": str(g.rowptr.dtype),
+            "graph_sha256": g.sha256(),
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "l2": "explicit 512 MiB L2 flush between timed steps; inputs (CSR 312 MB) and "
+                  "outputs exceed the 126 MB L2"}
+
+
 def workload_desc(cfg, g, k):
     c = gg.CONFIGS[cfg]
     kind = "planted-partition SBM" if c["kind"] == "pp" else "degree-corrected SBM"
@@ -85,13 +95,18 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
+def ncu_traffic(graph_sha):
+    """DRAM bytes per K2 launch from the committed `ncu --set full` capture
+    (profiles/k2_ncu_summary.json, written by scripts/summarize_ncu.py), used only when that
+    capture profiled THIS graph (same sha256); else (None, None)."""
     p = os.path.join(ROOT, "profiles", "k2_ncu_summary.json")
     try:
         d = json.load(open(p))
-        return d.get("dram_bytes_per_launch"), d
     except Exception:
         return None, None
+    if d.get("graph_sha256") != graph_sha:
+        return None, None
+    return d.get("dram_bytes_per_launch"), d
 
 
 class Clocks:
@@ -239,8 +254,7 @@ def main_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000 * secs / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg, g, len(deltas)), "n": g.n, "m": g.m,
-                       "graph_sha256": g.sha256(), "parallelism": "cpu oracle"},
+            "config": config_dict(cfg, g, deltas, 1),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": (f"each step = one of 64 row windows of config {cfg}: "
                                         "oracle scoring of the window's canonical edges + "
@@ -410,29 +424,42 @@ def main_b200(args):
                  "norm_cc": cl[idx][0] / n, "norm_edges": sl[idx][0] / m,
                  "norm_largest_cc": cl[idx][1] / n}
 
-    # ---- roofline of the dominant kernel (K2, oriented intersection), DESIGN.md Sec. 5
+    # ---- roofline of the dominant kernel (K2, oriented intersection), DESIGN.md Sec. 6
+    # algorithmic bytes of the pivot-staged intersection = 4 (m + S), S = sum_v
+    # d-(v) d+(v) (N+(u) read once per pivot, N+(v) once per in-edge), exact from this graph.
     S, dplus_max = orientation_stats(g)
     T = int(t.sum(dtype=torch.int64).item()) // 3
-    k2_bytes = 4 * (n + 1 + 4 * m + S + T)
+    k2_bytes = 4 * (m + S)
+    k2_bytes_ext = 4 * (n + 1 + 4 * m + S + T)
     k2_avg_s = statistics.mean(k2_ms) / 1000.0
     peak, peak_src = measured_peak()
     achieved = k2_bytes / k2_avg_s / 1e9
-    traffic, k2prof = ncu_traffic()
+    graph_sha = g.sha256()
+    traffic, k2prof = ncu_traffic(graph_sha)
     roofline = {"bound": "hbm", "kernel": "k2_intersect", "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "algorithmic_bytes_per_launch": k2_bytes, "peak_source": peak_src,
-                "k2_ms_avg": 1000 * k2_avg_s,
-                "frac_of_8000": achieved / 8000.0}
+                "algorithmic_bytes_per_launch": k2_bytes,
+                "algorithmic_model": "SURVEY 8(d) pivot-staged: 4*(m + S), S = sum_v d-(v)*d+(v)",
+                "peak_source": peak_src, "k2_ms_avg": 1000 * k2_avg_s,
+                "frac_of_8000": achieved / 8000.0,
+                "extended_model": {
+                    "bytes": k2_bytes_ext, "achieved": k2_bytes_ext / k2_avg_s / 1e9,
+                    "frac": k2_bytes_ext / k2_avg_s / 1e9 / peak,
+                    "model": "4*(n+1 + 4m + S + T): + rp_or per pivot and per out-neighbour, "
+                             "one count flush per slot, one RED per triangle"}}
     if traffic:
-        # SURVEY 8(d) figure 1: measured DRAM bytes per launch (committed ncu capture) over the
-        # live K2 time, against the measured copy peak and north_star's ~8 TB/s
+        # SURVEY 8(d) figure 1: measured DRAM bytes per launch (ncu capture of this graph, tag
+        # below) over the live K2 time, against the measured copy peak and north_star's ~8 TB/s
         dram_gbs = traffic / k2_avg_s / 1e9
+        roofline["traffic_source"] = {"tag": k2prof.get("tag"), "file": k2prof.get("source"),
+                                      "ncu_k2_duration": k2prof.get("duration")}
         roofline["dram"] = {"achieved": dram_gbs, "unit": "GB/s", "frac": dram_gbs / peak,
-                            "frac_of_8000": dram_gbs / 8000.0}
+                            "frac_of_8000": dram_gbs / 8000.0,
+                            "traffic_over_algorithmic": traffic / k2_bytes}
     if k2prof and k2prof.get("warp_inst_per_launch"):
-        # K2 is bound by instruction issue and load latency, not by DRAM:
-        # its warp instructions per launch (committed ncu capture) over the live K2 time,
-        # against 4 schedulers x SMs x max SM clock (one warp instruction per cycle each)
+        # K2 is co-limited by instruction issue and the L1/shared pipe: its
+        # warp instructions per launch (same capture) over the live K2 time, against 4
+        # schedulers x SMs x max SM clock (one warp instruction per cycle each)
         sms = torch.cuda.get_device_properties(0).multi_processor_count
         smax = clk.summary().get("sm_max_mhz") or 1965.0  # B200 max SM clock if unsampled
         peak_ginst = 4 * sms * smax / 1000.0
@@ -500,11 +527,7 @@ def main_b200(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg, g, k), "n": n, "m": m, "thresholds": deltas,
-                       "rowptr": str(g.rowptr.dtype), "graph_sha256": g.sha256(),
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "l2": "explicit 512 MiB L2 flush between timed steps; inputs (CSR 312 MB) "
-                             "and outputs exceed the 126 MB L2"},
+            "config": config_dict(cfg, g, deltas, world),
             "phases_ms": phases, "separate_calls_ms": separate, "selection": selection,
             "score_edges_per_s": world * m / (phases["score"] / 1000.0),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

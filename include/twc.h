@@ -20,7 +20,11 @@
  *  Memory.  Every array is caller-owned.  The library never allocates device memory: all
  *           scratch comes from a caller-provided device workspace whose size is given by the
  *           matching *_workspace_bytes query (cuBLAS style).  Workspaces must be 256-byte
- *           aligned.  Nothing is retained after a call returns; outputs must not alias inputs.
+ *           aligned.  DEVICE colidx must be 16-byte aligned and DEVICE rowptr aligned to
+ *           rowptr_bytes (the kernels read colidx with 16-byte vector loads; a view with an odd
+ *           storage offset, e.g. colidx[2:], is rejected with TWC_EINVAL rather than faulting).
+ *           HOST pointers of the *_host calls have no alignment requirement.
+ *           Nothing is retained after a call returns; outputs must not alias inputs.
  *  Streams. `stream` is a cudaStream_t (NULL = legacy default stream).  Device calls only
  *           enqueue work on it and return without synchronising (outputs are valid once the
  *           stream reaches them), except twc_validate_csr and the *_host calls, which
@@ -31,13 +35,16 @@
  *           unit; the *_host_async calls copy results back on a library-owned copy stream the
  *           same way.
  *  Errors.  Calls return a twc_status.  TWC_EINVAL: a null pointer where data is required
- *           (n > 0 or m > 0), n or m out of range, rowptr_bytes not in {4, 8}, NaN delta,
- *           k < 1.  TWC_EWORKSPACE: workspace too small or misaligned.  TWC_ECUDA: a CUDA launch
+ *           (n > 0 or m > 0), n or m out of range, rowptr_bytes not in {4, 8}, a misaligned
+ *           device colidx / rowptr, NaN delta, k < 1.  TWC_EWORKSPACE: workspace too small or misaligned.  TWC_ECUDA: a CUDA launch
  *           or runtime error (detail in twc_last_error()).  TWC_EGRAPH: only from
  *           twc_validate_csr.  Outputs are undefined on error; nothing aborts or throws.
  *           n = 0 or m = 0 is not an error: empty score arrays; labels[u] = u.
- *  Threads. Calls are re-entrant; there is no global state except the thread-local error
- *           string returned by twc_last_error().
+ *  Threads. Calls are re-entrant and may target any device (the current one).  Process-wide
+ *           state is limited to: the thread-local error string returned by twc_last_error(),
+ *           the launch counter of twc_kernel_launches(), per-(thread, device) side/copy streams
+ *           and events created on first use, and a mutex-guarded per-(device, kernel) cache of
+ *           the dynamic-shared-memory attribute and occupancy (the attribute is per device).
  */
 #ifndef TWC_H_
 #define TWC_H_
@@ -248,6 +255,21 @@ typedef enum { TWC_RULE_LARGEST_JUMP = 0, TWC_RULE_MAX_MODULARITY = 1 } twc_rule
 twc_status twc_select_threshold(const double *deltas, const int64_t *largest,
                                 const double *modularity, int32_t k, int64_t n,
                                 double jump_factor, int32_t *index, int32_t *rule);
+
+/* ---------------------------------------------------------------------------------------
+ * twc_sweep_norm_stats -- the three normalised statistics the threshold-selection study plots
+ * per sweep point ("norm # CC", "norm # edges", "norm |largest CC|"), from
+ * HOST copies of twc_partition_stats' counts and twc_sweep's stats:
+ *   counts[4k] (n_communities, largest, E_in, sum D_c^2 per partition), kept_stats[2k]
+ *   ({kept_edges, n_components} per threshold; NULL -> the norm-edges column is NaN),
+ *   norm[3k]:  norm[3j + 0] = counts[4j] / n        (number of communities / n)
+ *              norm[3j + 1] = kept_stats[2j] / m    (edges kept at delta_j / m)
+ *              norm[3j + 2] = counts[4j + 1] / n    (largest community / n)
+ * each one IEEE division of exact integers; NaN when the divisor is 0.  Host-only, no device
+ * work.  TWC_EINVAL: k < 1, n < 0, m < 0, NULL counts or norm.
+ * ------------------------------------------------------------------------------------- */
+twc_status twc_sweep_norm_stats(int64_t n, int64_t m, int32_t k, const int64_t *counts,
+                                const int64_t *kept_stats, double *norm);
 
 /* ---------------------------------------------------------------------------------------
  * twc_validate_csr -- checks the a0 precondition: rowptr[0] = 0, rowptr

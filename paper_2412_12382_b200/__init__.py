@@ -85,6 +85,7 @@ def load_library(path: str = LIB_PATH):
         "twc_partition_stats_workspace_bytes": (SZ, [I64, I64, I32]),
         "twc_partition_stats": (ctypes.c_int, [CP, P, I32, P, SZ, P, P, P]),
         "twc_select_threshold": (ctypes.c_int, [P, P, P, I32, I64, ctypes.c_double, P, P]),
+        "twc_sweep_norm_stats": (ctypes.c_int, [I64, I64, I32, P, P, P]),
         "twc_score_shard": (ctypes.c_int, [CP, I32, I32, P, SZ, P, P]),
         "twc_finish_scores": (ctypes.c_int, [CP, P, P, SZ, P, P, P]),
     }
@@ -133,10 +134,17 @@ def _stream(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def _workspace(nbytes, device, workspace=None):
+def _workspace(nbytes, device, workspace=None, stream=None):
+    """The caller's workspace if it is large enough, else a temporary one.  A temporary is
+    allocated on torch's current stream; when the library runs on another `stream`, the
+    temporary is tied to that stream (record_stream) so that the caching allocator does not hand
+    its memory out again before the enqueued kernels are done with it."""
     if workspace is not None and workspace.numel() >= nbytes:
         return workspace
-    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+    ws = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+    if stream is not None and stream != torch.cuda.current_stream(ws.device):
+        ws.record_stream(stream)
+    return ws
 
 
 def twc_score_workspace_bytes(n, m, rowptr_bytes=4):
@@ -174,7 +182,8 @@ def twc_score(rowptr, colidx, out=None, workspace=None, stream=None, events=None
     if out is None:
         out = tuple(torch.empty(m, dtype=torch.int32, device=dev) for _ in range(3))
     t, wedge, tw = out
-    ws = _workspace(lib.twc_score_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    ws = _workspace(lib.twc_score_workspace_bytes(n, m, rowptr.element_size()),
+                    dev, workspace, stream)
     ev = _events(events)
     _check(lib.twc_score_ex(ctypes.byref(g), _ptr(ws), ws.numel(), _ptr(t), _ptr(wedge), _ptr(tw),
                             _stream(stream), ev[0] if ev else None))
@@ -190,7 +199,8 @@ def twc_cluster(rowptr, colidx, tw, delta, labels=None, stats=None, workspace=No
         labels = torch.empty(n, dtype=torch.int32, device=dev)
     if stats is None:
         stats = torch.empty(2, dtype=torch.int64, device=dev)
-    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()),
+                    dev, workspace, stream)
     _check(lib.twc_cluster(ctypes.byref(g), _ptr(tw), float(delta), _ptr(ws), ws.numel(),
                            _ptr(labels), _ptr(stats), _stream(stream)))
     return labels, stats
@@ -211,7 +221,8 @@ def twc_sweep(rowptr, colidx, tw, deltas, labels=None, stats=None, workspace=Non
     if stats is None:
         stats = torch.empty((k, 2), dtype=torch.int64, device=dev)
     arr = (ctypes.c_double * k)(*deltas)
-    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()),
+                    dev, workspace, stream)
     ev = _events(events)
     _check(lib.twc_sweep_ex(ctypes.byref(g), _ptr(tw), ctypes.cast(arr, ctypes.c_void_p), k,
                             _ptr(ws), ws.numel(), _ptr(labels), _ptr(stats), _stream(stream),
@@ -242,7 +253,7 @@ def twc_score_sweep(rowptr, colidx, deltas, out=None, labels=None, stats=None, w
     t, wedge, tw = out
     arr = (ctypes.c_double * k)(*deltas)
     ws = _workspace(lib.twc_score_sweep_workspace_bytes(n, m, rowptr.element_size()), dev,
-                    workspace)
+                    workspace, stream)
     ev = _events(events)
     _check(lib.twc_score_sweep(ctypes.byref(g), ctypes.cast(arr, ctypes.c_void_p), k, _ptr(ws),
                                ws.numel(), _ptr(t), _ptr(wedge), _ptr(tw), _ptr(labels),
@@ -258,7 +269,7 @@ def twc_score_shard(rowptr, colidx, rank, world, out=None, workspace=None, strea
     if out is None:
         out = torch.empty(m, dtype=torch.int32, device=colidx.device)
     ws = _workspace(lib.twc_score_workspace_bytes(n, m, rowptr.element_size()), colidx.device,
-                    workspace)
+                    workspace, stream)
     _check(lib.twc_score_shard(ctypes.byref(g), int(rank), int(world), _ptr(ws), ws.numel(),
                                _ptr(out), _stream(stream)))
     return out
@@ -272,7 +283,8 @@ def twc_finish_scores(rowptr, colidx, t, out=None, workspace=None, stream=None):
     if out is None:
         out = tuple(torch.empty(m, dtype=torch.int32, device=dev) for _ in range(2))
     wedge, tw = out
-    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()),
+                    dev, workspace, stream)
     _check(lib.twc_finish_scores(ctypes.byref(g), _ptr(t), _ptr(ws), ws.numel(), _ptr(wedge),
                                  _ptr(tw), _stream(stream)))
     return wedge, tw
@@ -309,7 +321,8 @@ def twc_similarity(rowptr, colidx, t, kind, out=None, workspace=None, stream=Non
     dev = colidx.device
     if out is None:
         out = torch.empty(m, dtype=torch.float64, device=dev)
-    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()),
+                    dev, workspace, stream)
     _check(lib.twc_similarity(ctypes.byref(g), _ptr(t), SIM_KINDS[kind], _ptr(ws), ws.numel(),
                               _ptr(out), _stream(stream)))
     return out
@@ -328,7 +341,8 @@ def twc_sweep_f64(rowptr, colidx, score, deltas, labels=None, stats=None, worksp
     if stats is None:
         stats = torch.empty((k, 2), dtype=torch.int64, device=dev)
     arr = (ctypes.c_double * k)(*deltas)
-    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()),
+                    dev, workspace, stream)
     _check(lib.twc_sweep_f64(ctypes.byref(g), _ptr(score), ctypes.cast(arr, ctypes.c_void_p), k,
                              _ptr(ws), ws.numel(), _ptr(labels), _ptr(stats), _stream(stream)))
     return labels, stats
@@ -355,16 +369,14 @@ def twc_pipeline_host(rowptr, colidx, deltas, want_scores=True, out=None, worksp
                 out[key] = torch.empty(m, dtype=torch.int32, pin_memory=pin)
     arr = (ctypes.c_double * k)(*deltas)
     ws = _workspace(lib.twc_pipeline_workspace_bytes(n, m, rowptr.element_size(), k), dev,
-                    workspace)
+                    workspace, stream)
     fn = lib.twc_pipeline_host_async if asynchronous else lib.twc_pipeline_host
     _check(fn(ctypes.byref(g), ctypes.cast(arr, ctypes.c_void_p), k, _ptr(ws), ws.numel(),
               _ptr(out.get("t")), _ptr(out.get("wedge")), _ptr(out.get("tw")),
               _ptr(out["labels"]), _ptr(out["stats"]), _stream(stream)))
     if asynchronous:
-        # the device keeps using the workspace and the host buffers after this returns: tie the
-        # workspace to the stream for torch's allocator and keep the inputs referenced from out
-        if stream is not None and ws is not workspace:
-            ws.record_stream(stream)
+        # the device keeps using the workspace and the host buffers after this returns: the
+        # workspace is tied to `stream` (_workspace); keep the inputs referenced from out
         out["_inflight"] = (rowptr, colidx, ws)
     return out
 
@@ -402,7 +414,7 @@ def twc_partition_stats(rowptr, colidx, labels, counts=None, modularity=None, wo
     if modularity is None:
         modularity = torch.empty(k, dtype=torch.float64, device=dev)
     ws = _workspace(lib.twc_partition_stats_workspace_bytes(n, m, rowptr.element_size()), dev,
-                    workspace)
+                    workspace, stream)
     _check(lib.twc_partition_stats(ctypes.byref(g), _ptr(labels), k, _ptr(ws), ws.numel(),
                                    _ptr(counts), _ptr(modularity), _stream(stream)))
     return counts, modularity
@@ -423,6 +435,18 @@ def twc_select_threshold(deltas, largest, modularity, n, jump_factor=0.1):
     return int(idx.value), RULES[rule.value]
 
 
+def twc_sweep_norm_stats(n, m, counts, kept_stats=None):
+    """P:887-889's normalised sweep statistics from host int64 counts [k, 4] and kept_stats
+    [k, 2]: float64 [k, 3] = (n_communities / n, kept / m, largest / n) (computed in C)."""
+    lib = load_library()
+    counts = counts.to(torch.int64).contiguous().reshape(-1, 4)
+    k = counts.shape[0]
+    kept = None if kept_stats is None else kept_stats.to(torch.int64).contiguous().reshape(-1, 2)
+    norm = torch.empty((k, 3), dtype=torch.float64)
+    _check(lib.twc_sweep_norm_stats(int(n), int(m), k, _ptr(counts), _ptr(kept), _ptr(norm)))
+    return norm
+
+
 def sweep_report(rowptr, colidx, deltas, tw=None, jump_factor=0.1, stream=None):
     """The threshold-selection workflow: score once (unless tw is
     given), filter + label at every delta, the statistics of each partition and the selected
@@ -436,14 +460,13 @@ def sweep_report(rowptr, colidx, deltas, tw=None, jump_factor=0.1, stream=None):
     else:
         labels, stats = twc_sweep(rowptr, colidx, tw, deltas, stream=stream)
     counts, q = twc_partition_stats(rowptr, colidx, labels, stream=stream)
+    norm = twc_sweep_norm_stats(n, m, counts.cpu(), stats.cpu())
     counts, q, stats = counts.cpu().tolist(), q.cpu().tolist(), stats.cpu().tolist()
     pts = []
-    for d, c, qq, st in zip(deltas, counts, q, stats):
+    for d, c, qq, st, nm in zip(deltas, counts, q, stats, norm.tolist()):
         pts.append({"delta": float(d), "n_cc": c[0], "largest": c[1], "intra_edges": c[2],
                     "sum_deg_sq": c[3], "kept": st[0], "modularity": qq,
-                    "norm_cc": c[0] / n if n else float("nan"),
-                    "norm_edges": st[0] / m if m else float("nan"),
-                    "norm_largest_cc": c[1] / n if n else float("nan")})
+                    "norm_cc": nm[0], "norm_edges": nm[1], "norm_largest_cc": nm[2]})
     out = {"points": pts, "labels": labels}
     if n > 0:
         i, rule = twc_select_threshold(deltas, [p["largest"] for p in pts], q, n, jump_factor)
@@ -465,7 +488,8 @@ def twc_score_k4(rowptr, colidx, out=None, workspace=None, stream=None):
         out = tuple(torch.empty(m, dtype=torch.int32, device=dev) for _ in range(3)) + (
             torch.empty(m, dtype=torch.int64, device=dev),)
     t, wedge, tw, k4 = out
-    ws = _workspace(lib.twc_score_k4_workspace_bytes(n, m, rowptr.element_size()), dev, workspace)
+    ws = _workspace(lib.twc_score_k4_workspace_bytes(n, m, rowptr.element_size()),
+                    dev, workspace, stream)
     _check(lib.twc_score_k4(ctypes.byref(g), _ptr(ws), ws.numel(), _ptr(t), _ptr(wedge), _ptr(tw),
                             _ptr(k4), _stream(stream)))
     return t, wedge, tw, k4

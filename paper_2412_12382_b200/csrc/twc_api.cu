@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -48,7 +49,32 @@ int num_sms() {
     return v;
 }
 
-static twc_status check_csr(const twc_csr* g, bool need_ptrs = true) {
+int kernel_setup(const void* fn, int threads, size_t smem) {
+    struct Entry {
+        int dev;
+        const void* fn;
+        size_t smem;
+        int occ;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry& e : cache)
+        if (e.dev == dev && e.fn == fn && e.smem == smem) return e.occ;
+    int occ = 0;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
+    if (occ < 1) {
+        cudaGetLastError();  // a failed query must not leak into the launch status
+        occ = 1;
+    }
+    cache.push_back({dev, fn, smem, occ});
+    return occ;
+}
+
+static twc_status check_csr(const twc_csr* g, bool need_ptrs = true, bool device_ptrs = true) {
     if (!g) return fail(TWC_EINVAL, "graph descriptor is NULL");
     if (g->n < 0 || g->n >= ((int64_t)1 << 31)) return fail(TWC_EINVAL, "n=%lld out of range", (long long)g->n);
     if (g->m < 0 || g->m >= ((int64_t)1 << 31)) return fail(TWC_EINVAL, "m=%lld out of range", (long long)g->m);
@@ -59,6 +85,10 @@ static twc_status check_csr(const twc_csr* g, bool need_ptrs = true) {
     if (g->m > 0 && g->n == 0) return fail(TWC_EINVAL, "m > 0 with n == 0");
     if (need_ptrs && g->n > 0 && !g->rowptr) return fail(TWC_EINVAL, "rowptr is NULL");
     if (need_ptrs && g->m > 0 && !g->colidx) return fail(TWC_EINVAL, "colidx is NULL");
+    if (device_ptrs && g->m > 0 && reinterpret_cast<uintptr_t>(g->colidx) % 16)
+        return fail(TWC_EINVAL, "device colidx must be 16-byte aligned (vector loads)");
+    if (device_ptrs && g->n > 0 && reinterpret_cast<uintptr_t>(g->rowptr) % g->rowptr_bytes)
+        return fail(TWC_EINVAL, "device rowptr must be %d-byte aligned", g->rowptr_bytes);
     return TWC_OK;
 }
 
@@ -409,7 +439,7 @@ twc_status twc_pipeline_host_async(const twc_csr* gh, const double* deltas_host,
                                    void* ws, size_t ws_bytes, int32_t* t, int32_t* wedge,
                                    int32_t* tw, int32_t* labels, int64_t* stats, void* stream) {
     g_err.clear();
-    twc_status st = check_csr(gh);
+    twc_status st = check_csr(gh, true, false);  // host buffers: copied to aligned device memory
     if (st) return st;
     if (k < 1 || k > 1024) return fail(TWC_EINVAL, "k=%d must be in [1, 1024]", k);
     if (!deltas_host) return fail(TWC_EINVAL, "deltas_host is NULL");
@@ -551,6 +581,21 @@ twc_status twc_partition_stats(const twc_csr* g, const int32_t* labels, int32_t 
                                             reinterpret_cast<long long*>(counts), modularity, &bad, s);
     if (e != cudaSuccess) return cuda_status(e, "twc_partition_stats");
     if (bad) return fail(TWC_EINVAL, "a label lies outside [0, n)");
+    return TWC_OK;
+}
+
+twc_status twc_sweep_norm_stats(int64_t n, int64_t m, int32_t k, const int64_t* counts,
+                                const int64_t* kept_stats, double* norm) {
+    g_err.clear();
+    if (k < 1 || n < 0 || m < 0) return fail(TWC_EINVAL, "k=%d n=%lld m=%lld", k, (long long)n,
+                                             (long long)m);
+    if (!counts || !norm) return fail(TWC_EINVAL, "counts or norm is NULL");
+    const double nan = NAN;
+    for (int j = 0; j < k; ++j) {
+        norm[3 * j + 0] = n ? (double)counts[4 * j] / (double)n : nan;
+        norm[3 * j + 1] = (m && kept_stats) ? (double)kept_stats[2 * j] / (double)m : nan;
+        norm[3 * j + 2] = n ? (double)counts[4 * j + 1] / (double)n : nan;
+    }
     return TWC_OK;
 }
 

@@ -26,6 +26,13 @@ struct Carver {
 
 int num_sms();
 
+// Launch set-up of a kernel with dynamic shared memory (K2, K2h, K4 groups; K2h needs more
+// than 48 KB): sets cudaFuncAttributeMaxDynamicSharedMemorySize on the CURRENT device (the
+// attribute is per device) once per (device, kernel, smem) and returns the resident blocks per
+// SM (>= 1).  Thread-safe; the cache is the library's only process-wide state besides the
+// launch counter and the per-thread error string.
+int kernel_setup(const void* fn, int threads, size_t smem);
+
 // Launch accounting (twc_kernel_launches) and optional phase events (twc_*_ex).
 void count_launches(int k);
 inline void record(cudaEvent_t* ev, int i, cudaStream_t s) {

@@ -321,12 +321,7 @@ template <int W>
 static void launch_k4_groups(int64_t n, const int* rp_or, const int* col_or,
                              unsigned long long* k4_or, int* work, cudaStream_t s) {
     const size_t smem = kK4Warps * sizeof(K4GroupSmem<W>);
-    static int occ = 0;
-    if (occ == 0) {
-        cudaFuncSetAttribute(k4_groups<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_groups<W>, kK4Warps * 32, smem);
-        if (occ < 1) occ = 1;
-    }
+    const int occ = kernel_setup((const void*)k4_groups<W>, kK4Warps * 32, smem);
     const int sms = num_sms();
     const int64_t warps = (int64_t)sms * occ * kK4Warps;
     const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(32, n / (8 * warps)));

@@ -36,10 +36,11 @@ __global__ void k0_degrees(int64_t n, const RP* __restrict__ rowptr, int* __rest
 //   * the canonical id of an upper slot p is  #upper(q < p)    (S:66-69 order);
 //   * rp_or[u] = #out(q < rowptr[u]),  eoff[u] = #upper(q < rowptr[u]);
 //   * so the oriented slot of an aligned edge (out and upper) is #out before its upper slot.
-// K1 is one pass over tiles of kSlotTile slots (8 consecutive slots per thread, one row search
-// per thread, then a walk) with a block scan and a decoupled look-back across tiles for the
-// two prefix counts; it also stores per-32-slot word bits and exclusive prefixes so that K1r
-// can derive rp_or/eoff for every row with one lookup.
+// K1 runs over tiles of kSlotTile slots (8 consecutive slots per thread): K1a computes the bits
+// and per-tile counts, one block scans the tile counts, K1b scatters col_or and stores per-32-
+// slot exclusive prefixes so that K1r and K3 derive any slot's oriented / canonical index with
+// one lookup and a popc.  (A single pass with a decoupled look-back was measured slower,
+// DESIGN.md Sec. 4.)
 constexpr int kSlotThreads = 256;
 constexpr int kSlotItems = 8;
 constexpr int kSlotTile = kSlotThreads * kSlotItems;  // 2048 slots
@@ -409,7 +410,7 @@ __device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int head, int
 
 // Expand records [rhead, rhead + cnt) (cnt <= 32, lane i takes record rhead + i) into the
 // candidate ring at tail while they fit; returns the number of records consumed (a prefix; at
-// least 24 when fewer than 32 candidates are pending).
+// least 12 when fewer than 32 candidates are pending: a record holds at most Q = 8).
 template <int Q>
 __device__ __forceinline__ int k2_expand(K2WarpSmem& S, int lane, int rhead, int cnt, int head,
                                          int& tail) {
@@ -995,7 +996,7 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     const int64_t m2 = 2 * m;
     const int64_t nst = (m2 + kSlotTile - 1) / kSlotTile;
     record(ev, 0, s);
-    // a1 + a2: degrees, orientation, oriented CSR (one pass with a decoupled look-back)
+    // a1 + a2: degrees, orientation, oriented CSR (bits + tile counts, tile scan, scatter, rows)
     k0_degrees<RP><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rowptr, w.deg);
     count_launches(1);
     tile_rows<RP>(rowptr, (int)n, m2, kSlotTile, w.ftrow, s);
@@ -1024,14 +1025,7 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     // a3: oriented intersection
     {
         const size_t smem = kK2Warps * sizeof(K2WarpSmem);
-        static int occ = 0;
-        if (occ == 0) {
-            cudaFuncSetAttribute(k2_intersect<kOct>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_intersect<kOct>, kK2Warps * 32,
-                                                          smem);
-            if (occ < 1) occ = 1;
-        }
+        const int occ = kernel_setup((const void*)k2_intersect<kOct>, kK2Warps * 32, smem);
         record(ev, 1, s);
         // hub pivots (|N+(u)| > kGroupSlots, one per CTA) run on a library-owned side stream,
         // forked from and joined back to s: they start first (the largest tasks) and the
@@ -1045,12 +1039,8 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         }
         k2_find_hubs<<<(unsigned)((n + 255) / 256), 256, 0, sh>>>(n, w.rp_or, w.hubs, w.nhubs,
                                                                  range);
-        static int hub_set = 0;
         const size_t hsmem = sizeof(K2HubSmem);
-        if (!hub_set) {
-            cudaFuncSetAttribute(k2_hubs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
-            hub_set = 1;
-        }
+        kernel_setup((const void*)k2_hubs, kK2Warps * 32, hsmem);
         k2_hubs<<<sms * 2, kK2Warps * 32, hsmem, sh>>>(w.rp_or, w.col_or, w.hubs, w.nhubs,
                                                         w.work + 1, w.t_or);
         if (ax) cudaEventRecord(ax->join, sh);

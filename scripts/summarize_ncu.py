@@ -58,6 +58,19 @@ def to_bytes(val, unit):
     return v * scale.get(unit, 1)
 
 
+def bench_identity(tag):
+    """config / graph identity of the bench line captured in the same gpurun (gpurun_out/
+    bench_TAG.json), so bench.py only uses this capture's DRAM bytes for the same graph."""
+    p = os.path.join(ROOT, "gpurun_out", f"bench_{tag}.json")
+    try:
+        d = json.loads(open(p).read().strip().splitlines()[-1])
+        c = d["config"]
+        return {"graph_sha256": c.get("graph_sha256"), "n": c.get("n"), "m": c.get("m"),
+                "workload": c.get("workload"), "bench_line": f"profiles/{tag}_bench.json"}
+    except Exception:
+        return {}
+
+
 def full_summary(tag, rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
@@ -93,7 +106,7 @@ def full_summary(tag, rep):
                   "warp_inst_per_launch": float(r[col["smsp__inst_executed.sum"]].replace(",", "")),
                   "issue_active_pct": float(r[col["smsp__issue_active.avg.pct_of_peak_sustained_active"]]),
                   "duration": r[col["gpu__time_duration.sum"]] + " " + units[col["gpu__time_duration.sum"]],
-                  "source": f"profiles/{tag}_ncu_full.md"}
+                  "source": f"profiles/{tag}_ncu_full.md", **bench_identity(tag)}
     with open(os.path.join(PROF, f"{tag}_ncu_full.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     if k2:

@@ -42,7 +42,7 @@ def test_workspace_queries_are_host_only(lib):
     assert lib.twc_pipeline_workspace_bytes(10, 10, 3, 1) == 0
 
 
-def _csr(n, m, rb=4, rowptr=1, colidx=2):
+def _csr(n, m, rb=4, rowptr=256, colidx=512):  # fake, suitably aligned device pointers
     return twc._Csr(n, m, ctypes.c_void_p(rowptr), rb, ctypes.c_void_p(colidx))
 
 
@@ -78,6 +78,28 @@ def test_argument_errors_before_device(lib):
     assert lib.twc_partition_stats(ctypes.byref(big), P(1), 1, None, 0, P(1), None, None) == twc.TWC_EINVAL
     assert b"4m^2" in lib.twc_last_error()
     assert lib.twc_partition_stats_workspace_bytes(4_000_000, 35_000_000, 8) >= 12 * 4_000_000
+    # alignment: device colidx 16-byte, rowptr rowptr_bytes-aligned, else EINVAL
+    for rp, ci, rb in [(256, 516, 4), (256, 520, 8), (258, 512, 4), (260, 512, 8)]:
+        g = _csr(10, 5, rb=rb, rowptr=rp, colidx=ci)
+        assert lib.twc_score(ctypes.byref(g), P(256), 1 << 30, P(1), P(1), P(1), None) == twc.TWC_EINVAL
+        assert b"aligned" in lib.twc_last_error()
+    # host pipeline: host pointers need no alignment (copied into the aligned workspace)
+    g = _csr(10, 5, rb=4, rowptr=258, colidx=516)
+    assert lib.twc_pipeline_host_async(ctypes.byref(g), ctypes.cast(d, P), 1, None, 0, None, None,
+                                       None, None, None, None) == twc.TWC_EWORKSPACE
+
+
+def test_sweep_norm_stats_host(lib):
+    import torch
+    counts = torch.tensor([[4, 7, 30, 900], [10, 1, 0, 100]], dtype=torch.int64)
+    kept = torch.tensor([[40, 4], [0, 10]], dtype=torch.int64)
+    norm = twc.twc_sweep_norm_stats(10, 50, counts, kept)
+    assert norm.tolist() == [[4 / 10, 40 / 50, 7 / 10], [10 / 10, 0 / 50, 1 / 10]]
+    norm = twc.twc_sweep_norm_stats(0, 0, counts, None)
+    assert torch.isnan(norm).all()
+    P = ctypes.c_void_p
+    assert lib.twc_sweep_norm_stats(10, 5, 0, P(1), None, P(1)) == twc.TWC_EINVAL
+    assert lib.twc_sweep_norm_stats(10, 5, 1, None, None, P(1)) == twc.TWC_EINVAL
 
 
 def _select(lib, deltas, largest, q, n, jump=0.1):

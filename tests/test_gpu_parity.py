@@ -331,3 +331,36 @@ def test_config_parity_full_size(oracle_mod, config):
     deltas = harness.thresholds(config, tw)
     assert_cluster_parity(oracle_mod, g, tw, deltas)
     fused_parity(oracle_mod, g, deltas, ot)
+
+
+def test_misaligned_colidx_view_rejected():
+    """a contiguous view with an odd storage offset must come back as TWC_EINVAL, not
+    as a misaligned-address fault that poisons the context."""
+    g = gg.complete(40)
+    rp, ci = harness.to_device(g)
+    buf = torch.empty(ci.numel() + 1, dtype=torch.int32, device=ci.device)
+    buf[1:].copy_(ci)
+    with pytest.raises(twc.TwcError) as ei:
+        twc.twc_score(rp, buf[1:])
+    assert ei.value.status == twc.TWC_EINVAL
+    t, _, _ = twc.twc_score(rp, ci)        # the context is still healthy
+    torch.cuda.synchronize()
+    assert int(t.min()) == 38 and int(t.max()) == 38
+
+
+def test_temporary_workspace_on_side_stream(oracle_mod):
+    """a temporary workspace used on a non-current stream is tied to that stream, so
+    allocations made on the current stream meanwhile cannot reuse it."""
+    g = gg.erdos_renyi(2000, 0.02, seed=5)
+    ot, ow, otw = oracle_mod.score(g)
+    rp, ci = harness.to_device(g)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    outs = []
+    for _ in range(4):
+        t, w, tw = twc.twc_score(rp, ci, stream=side)      # no workspace: a temporary each call
+        junk = torch.full((1 << 22,), -1, dtype=torch.int32, device=ci.device)  # current stream
+        outs.append((t, w, tw, junk))
+    torch.cuda.synchronize()
+    for t, w, tw, _ in outs:
+        assert np.array_equal(t.cpu().numpy(), ot) and np.array_equal(tw.cpu().numpy(), otw)
