@@ -64,6 +64,8 @@ def _load():
         lib.oracle_select.restype = ctypes.c_int32
         lib.oracle_k4.argtypes = [I64, P, P, P]
         lib.oracle_k4.restype = ctypes.c_int
+        lib.oracle_times.argtypes = [P]
+        lib.oracle_times.restype = None
         lib.oracle_max_threads.restype = ctypes.c_int
         lib.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = lib
@@ -82,6 +84,14 @@ def _csr(g):
 
 def set_threads(k: int) -> None:
     _load().oracle_set_threads(int(k))
+
+
+def last_times():
+    """Steady-clock seconds of the last score() (O2) and of the filter (O3) and BFS (O4) parts of
+    the last cluster() -- SURVEY 8(d) oracle timing; measurement only."""
+    out = np.zeros(3, dtype=np.float64)
+    _load().oracle_times(_ptr(out))
+    return {"O2": float(out[0]), "O3": float(out[1]), "O4": float(out[2])}
 
 
 def max_threads() -> int:

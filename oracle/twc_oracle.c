@@ -49,12 +49,25 @@
  * writes, deterministic).  Everything is int32/int64 integer arithmetic, so there is no
  * rounding anywhere (reading C18).  The comparison (double)TW < delta is exact (|TW| < 2^53).
  */
+#define _POSIX_C_SOURCE 199309L
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
+
+/* Timing only (SURVEY 8(d) "Oracle timing": O2, O3 and O4 timed separately, excluding load):
+ * steady-clock seconds of the last oracle_score (O2) and of the filter (O3) and BFS (O4) parts
+ * of the last oracle_cluster.  No arithmetic of the method depends on these. */
+static double g_times[3];
+static double now_s(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+void oracle_times(double *out) { out[0] = g_times[0]; out[1] = g_times[1]; out[2] = g_times[2]; }
 
 int oracle_max_threads(void) {
 #ifdef _OPENMP
@@ -93,6 +106,7 @@ int oracle_score(int64_t n, const int64_t *rowptr, const int32_t *colidx,
                  int64_t u_begin, int64_t u_end,
                  int32_t *t, int32_t *wedge, int32_t *tw) {
     if (n <= 0) return 0;
+    const double t0 = now_s();
     int64_t *eoff = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
     if (!eoff) return 1;
     canonical_offsets(n, rowptr, colidx, eoff);
@@ -123,6 +137,7 @@ int oracle_score(int64_t n, const int64_t *rowptr, const int32_t *colidx,
         }
     }
     free(eoff);
+    g_times[0] = now_s() - t0;
     return 0;
 }
 
@@ -138,6 +153,7 @@ int oracle_cluster(int64_t n, const int64_t *rowptr, const int32_t *colidx,
         return 0;
     }
     /* line 1 of Alg. 1: remove e iff sim(e) < delta -- materialise the kept graph */
+    const double t0 = now_s();
     int64_t *kdeg = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
     if (!kdeg) return 1;
     int64_t c = 0, kept = 0;
@@ -166,6 +182,7 @@ int oracle_cluster(int64_t n, const int64_t *rowptr, const int32_t *colidx,
             ++c;
         }
     /* line 2 of Alg. 1: connected components, by BFS in ascending start id */
+    const double t1 = now_s();
     for (int64_t u = 0; u < n; ++u) labels[u] = -1;
     int64_t ncomp = 0;
     for (int64_t s = 0; s < n; ++s) {
@@ -184,6 +201,8 @@ int oracle_cluster(int64_t n, const int64_t *rowptr, const int32_t *colidx,
     }
     if (stats) { stats[0] = kept; stats[1] = ncomp; }
     free(kdeg); free(fill); free(kadj); free(queue);
+    g_times[1] = t1 - t0;
+    g_times[2] = now_s() - t1;
     return 0;
 }
 
