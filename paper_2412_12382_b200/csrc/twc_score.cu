@@ -13,8 +13,6 @@
 // count arrays, which one int32 array plus atomics avoids on a GPU.  DESIGN.md Sec. 4.
 #include <algorithm>
 #include <climits>
-#include <cstdio>
-#include <cstdlib>
 #include <vector>
 
 #include "twc_common.cuh"
@@ -340,7 +338,7 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
 //    sector of col_or (covering [start & ~7, end)).  The groups of the 32 slots are flattened
 //    across the lanes (exclusive scan of the group counts; the segment owning a group is found
 //    with one __reduce_or_sync bit mask + one smem lookup), so each lane reads one aligned
-//    sector (two 16-byte loads) of one N+(v) and a warp reads a contiguous run.  The per-lane
+//    sector (one 256-bit LDG.E.256) of one N+(v) and a warp reads a contiguous run.  The per-lane
 //    segment record {start & ~7 - 8 * first group, end, tag, start} gives a group's slots with
 //    one 16-byte smem load; loads are clamped into the list, so loads and hashes run
 //    unpredicated and one validity mask (start <= slot < end) is applied per group;
@@ -365,7 +363,7 @@ constexpr int kFilterBits = 1 << kFilterLog;
 constexpr int kFilterWords = kFilterBits / 32;
 constexpr int kPivotChunk = 32;
 constexpr int kQuad = 4;  // K2h: items per lane (one aligned 16-byte load)
-constexpr int kOct = 8;   // K2: items per lane (one aligned 32-byte sector, two 16-byte loads)
+constexpr int kOct = 8;   // K2: items per lane (one aligned 32-byte sector, one 256-bit load)
 constexpr int kRing = 128;  // candidate ring (an expansion stops before it would overflow)
 constexpr int kRec = 64;    // record ring, >= 31 + 32 pending records
 constexpr unsigned kFiltK = 2654435761u;
@@ -383,16 +381,6 @@ struct K2WarpSmem {
 };
 
 __device__ __forceinline__ unsigned filter_word(unsigned x) { return x >> (32 - kFilterLog + 5); }
-
-// Conflict-free filters (FM > 0): FM independent 1,024-bit filters of 32 words each.  With one
-// word per bank, a warp-wide probe of one filter is conflict-free whatever the lanes' items
-// (two lanes in the same bank read the same word: a broadcast).  Filter f sits in words
-// [32 f, 32 f + 32): word = top 5 bits of h = x * K_f, bit = h & 31 (f = 0) or bits 22..26.
-constexpr unsigned kFiltK1 = 0x85ebca6bu, kFiltK2 = 0xc2b2ae35u;
-__device__ __forceinline__ unsigned cf_hash(int f, int x) {
-    return (unsigned)x * (f == 0 ? kFiltK : f == 1 ? kFiltK1 : kFiltK2);
-}
-__device__ __forceinline__ unsigned cf_bit(int f, unsigned h) { return f == 0 ? h : (h >> 22); }
 
 // One aligned 32-byte sector of col_or per lane: a single 256-bit load (LDG.E.256, sm_100)
 // instead of two 128-bit loads touching the same lines twice.
@@ -475,7 +463,7 @@ __device__ __forceinline__ void k2_drain(K2WarpSmem& S, int lane, int keep, int 
 }
 
 // range: NULL (all pivots) or device {u_lo, u_hi} of a shard (the queue starts at u_lo)
-template <int Q, bool V256, int FM>
+template <int Q>
 __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int chunk,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
@@ -510,21 +498,13 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
             const int B = __shfl_sync(FULL, e_l, np - 1);
             if (lane == 0) S.prp[0] = A;
             if (lane < np) S.prp[lane + 1] = e_l;
-            for (int i = lane; i < (FM ? 32 * FM : kFilterWords); i += 32) S.filt[i] = 0u;
+            for (int i = lane; i < kFilterWords; i += 32) S.filt[i] = 0u;
             __syncwarp();
             for (int i = lane; i < B - A; i += 32) {
                 const int x = __ldcs(col_or + A + i);  // read once: staged, not kept in L1
                 S.list[i] = x;
-                if (FM == 0) {
-                    const unsigned h = (unsigned)x * kFiltK;
-                    atomicOr(&S.filt[filter_word(h)], 1u << (h & 31));
-                } else {
-#pragma unroll
-                    for (int f = 0; f < FM; ++f) {
-                        const unsigned h = cf_hash(f, x);
-                        atomicOr(&S.filt[32 * f + (h >> 27)], 1u << (cf_bit(f, h) & 31));
-                    }
-                }
+                const unsigned h = (unsigned)x * kFiltK;
+                atomicOr(&S.filt[filter_word(h)], 1u << (h & 31));
             }
             __syncwarp();
             int head = 0, tail = 0;    // candidate ring
@@ -567,11 +547,11 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                     const int jj = mine ? own : cur;
                     const int4 sg = S.seg[jj];
                     const int sv0 = sg.x + Q * (k0 + lane);  // 4Q-byte aligned
-                    // Q / 4 aligned 16-byte loads per lane (clamped to the list's last group)
+                    // the aligned sector of this lane (clamped to the list's last group)
                     const int4* src = reinterpret_cast<const int4*>(
                         col_or + min(sv0, (sg.y - 1) & ~(Q - 1)));
                     int w[Q];
-                    if (V256 && Q == 8) {
+                    if (Q == 8) {  // one 256-bit load (LDG.E.256) per lane
                         ldg_sector(reinterpret_cast<const int*>(src), *reinterpret_cast<int(*)[8]>(w));
                     } else {
 #pragma unroll
@@ -581,38 +561,15 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                         }
                     }
                     unsigned cm = 0;
-                    if (FM == 0) {
 #pragma unroll
-                        for (int e = 0; e < Q; ++e) {
-                            const unsigned x = (unsigned)w[e] * kFiltK;
-                            // opaque word index: keeps ptxas from folding the shift into
-                            // (x >> 22) & 0x3fc + base (3 ops) so the address is SHF + LEA
-                            unsigned fw = filter_word(x);
-                            asm("" : "+r"(fw));
-                            const unsigned word = S.filt[fw];
-                            cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
-                        }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < Q; ++e) {  // filter 0: every item
-                            const unsigned x = (unsigned)w[e] * kFiltK;
-                            const unsigned word = S.filt[x >> 27];
-                            cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
-                        }
-#pragma unroll
-                        for (int f = 1; f < FM; ++f) {  // filter f: the items that passed so far
-                            unsigned c2 = 0;
-#pragma unroll
-                            for (int e = 0; e < Q; ++e) {
-                                if ((cm >> e) & 1u) {
-                                    const unsigned x = cf_hash(f, w[e]);
-                                    const unsigned word = S.filt[32 * f + (x >> 27)];
-                                    c2 |= __funnelshift_r(word, word, cf_bit(f, x) - (unsigned)e) &
-                                          (1u << e);
-                                }
-                            }
-                            cm = c2;
-                        }
+                    for (int e = 0; e < Q; ++e) {
+                        const unsigned x = (unsigned)w[e] * kFiltK;
+                        // opaque word index: keeps ptxas from folding the shift into
+                        // (x >> 22) & 0x3fc + base (3 ops) so the address is SHF + LEA
+                        unsigned fw = filter_word(x);
+                        asm("" : "+r"(fw));
+                        const unsigned word = S.filt[fw];
+                        cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
                     }
                     // valid entries: sg.w <= sv0 + e < sg.y
                     cm &= ((1u << min(max(sg.y - sv0, 0), Q)) - 1u) &
@@ -1040,23 +997,6 @@ static AuxStream* aux_stream() {
     return &lanes.back();
 }
 
-// K2 variant (measurement A/B): TWC_K2="<v256>,<fm>" selects the 256-bit
-// sector load and the filter mode (0 = one 8,192-bit filter, 2 / 3 = conflict-free 1,024-bit
-// filters); read once per process.
-typedef void (*K2Fn)(int64_t, int, const int*, const int*, int*, int*, const int*, const int2*);
-static K2Fn k2_variant() {
-    static const K2Fn fn = [] {
-        int v = 0, fm = 0;
-        if (const char* e = getenv("TWC_K2")) sscanf(e, "%d,%d", &v, &fm);
-        if (v && fm == 2) return (K2Fn)k2_intersect<kOct, true, 2>;
-        if (v && fm == 3) return (K2Fn)k2_intersect<kOct, true, 3>;
-        if (!v && fm == 2) return (K2Fn)k2_intersect<kOct, false, 2>;
-        if (v) return (K2Fn)k2_intersect<kOct, true, 0>;
-        return (K2Fn)k2_intersect<kOct, false, 0>;
-    }();
-    return fn;
-}
-
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
@@ -1098,8 +1038,7 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     // a3: oriented intersection
     {
         const size_t smem = kK2Warps * sizeof(K2WarpSmem);
-        const K2Fn k2fn = k2_variant();
-        const int occ = kernel_setup((const void*)k2fn, kK2Warps * 32, smem);
+        const int occ = kernel_setup((const void*)k2_intersect<kOct>, kK2Warps * 32, smem);
         record(ev, 1, s);
         // hub pivots (|N+(u)| > kGroupSlots, one per CTA) run on a library-owned side stream,
         // forked from and joined back to s: they start first (the largest tasks) and the
@@ -1122,8 +1061,8 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
         // warp several grabs (small dense graphs), so the queue still balances the load
         const int64_t warps = (int64_t)sms * occ * kK2Warps;
         const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(kPivotChunk, n / (8 * warps)));
-        k2fn<<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or, w.t_or, w.work,
-                                                    range, w.vinfo);
+        k2_intersect<kOct><<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or,
+                                                                   w.t_or, w.work, range, w.vinfo);
         if (ax) cudaStreamWaitEvent(s, ax->join, 0);
         count_launches(3);
         record(ev, 2, s);
