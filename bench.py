@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # N > 1: NCCL on a B200 node.  gloo + --same-device runs every rank on cuda:0 with host-side
+    # exchanges (a functional check of this code path on a one-GPU box, not a measurement)
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--same-device", action="store_true")
     return ap.parse_args()
 
 
@@ -60,7 +64,8 @@ def config_dict(cfg, g, deltas, world):
     return {"workload": workload_desc(cfg, g, len(deltas)), "n": g.n, "m": g.m,
             "thresholds": list(deltas), "rowptr": str(g.rowptr.dtype),
             "graph_sha256": g.sha256(),
-            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"one graph split over {world} GPUs (SURVEY 8(e) row ranges, NCCL "
+                            "exchanges)") if world > 1 else "single GPU",
             "l2": "explicit 512 MiB L2 flush between timed steps; inputs (CSR 312 MB) and "
                   "outputs exceed the 126 MB L2"}
 
@@ -557,10 +562,126 @@ def main_b200(args):
     return 0
 
 
+def main_b200_dist(args):
+    """N > 1 (torchrun, one process per GPU): ONE graph split over the N GPUs (SURVEY 8(e);
+    paper_2412_12382_b200/dist.py): every rank runs the six twc_dist_* phases on its row range
+    with the three NCCL exchanges between them.  Strong scaling: value = m * K / (max over ranks
+    of the device time of K steps).  DESIGN.md Sec. 7."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_12382_b200 as twc
+    from paper_2412_12382_b200 import build as twc_build
+    from paper_2412_12382_b200 import dist as tdist
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ.get("RANK", "0"))
+    local = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
+    if rank == 0:
+        twc_build.build()
+    dist.barrier()
+    twc.load_library()
+    cfg = args.config
+    g = gg.config_graph(cfg)
+    n, m = g.n, g.m
+    rp, ci = harness.to_device(g, dev)
+    stream = torch.cuda.current_stream()
+    deltas = harness.SWEEP_GRID if cfg == 5 else None
+    if deltas is None:  # the thresholds of the smaller configs come from the scores
+        _, _, tw0 = twc.twc_score(rp, ci)
+        deltas = harness.thresholds(cfg, tw0.cpu().numpy())
+    k = len(deltas)
+    comm = tdist.TorchComm()
+    st = tdist.DistRank(rp, ci, deltas, rank, world)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        return tdist.run_phases([st], comm)[0]
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    K = args.steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    l0 = twc.twc_kernel_launches()
+    dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        wall0 = time.perf_counter()
+        for i in range(K):
+            flush.zero_()
+            starts[i].record(stream)
+            info = step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    dist.barrier()
+    launches = (twc.twc_kernel_launches() - l0) / K
+    total_s = harness.max_over_ranks(sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / 1000.0,
+                                     dev if args.backend == "nccl" else None)
+    value = m * K / total_s
+    # end to end: every rank copies the CSR in from pinned host memory, runs the step and copies
+    # its slice of TW back; rank 0 also copies the labels and stats of all k thresholds back
+    rows, cb = tdist.slice_bounds(rp, ci, world)
+    c0, c1 = cb[rank], cb[rank + 1]
+    rp_h = torch.from_numpy(np.ascontiguousarray(g.rowptr)).pin_memory()
+    ci_h = torch.from_numpy(np.ascontiguousarray(g.colidx)).pin_memory()
+    tw_h = torch.empty(max(1, c1 - c0), dtype=torch.int32, pin_memory=True)
+    lab_h = torch.empty((k, n), dtype=torch.int32, pin_memory=True)
+    st_h = torch.empty((k, 2), dtype=torch.int64, pin_memory=True)
+    E = max(4, min(K, 10))
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(E):
+        rp.copy_(rp_h, non_blocking=True)
+        ci.copy_(ci_h, non_blocking=True)
+        step()
+        tw_h[:c1 - c0].copy_(st.tw[c0:c1], non_blocking=True)
+        if rank == 0:
+            lab_h.copy_(st.labels, non_blocking=True)
+            st_h.copy_(st.stats, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_s = harness.max_over_ranks(e0.elapsed_time(e1) / 1000.0 / E,
+                                 dev if args.backend == "nccl" else None)
+    csr_bytes = rp_h.numel() * rp_h.element_size() + ci_h.numel() * 4
+    e2e = {"value": m / e_s, "unit": UNIT, "h2d_bytes_per_step": world * csr_bytes,
+           "d2h_bytes_per_step": 4 * m + 4 * k * n + 16 * k, "ms_per_step": 1000 * e_s,
+           "steps": E, "api": "paper_2412_12382_b200.dist.score_sweep path (DistRank.run)",
+           "note": "every rank copies the whole CSR in; the TW slices (all ranks) and the "
+                   "labels (rank 0) come back"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * total_s / K,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int32", "data": "synthetic", "config": config_dict(cfg, g, deltas, world),
+            "exchange": {"backend": args.backend, "records_last_step_rank0": info,
+                         "slice_rows_rank0": [rows[0], rows[1]]},
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "wall_s_timed": wall,
+            "roofline": None, "cpu_baseline": None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return main_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return main_b200_dist(args)
     return main_b200(args)
 
 

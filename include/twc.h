@@ -215,6 +215,70 @@ twc_status twc_finish_scores(const twc_csr *g, const int32_t *t, void *workspace
                              size_t workspace_bytes, int32_t *wedge, int32_t *tw, void *stream);
 
 /* ---------------------------------------------------------------------------------------
+ * twc_dist_* -- the whole hot path (score + k-threshold sweep) of ONE graph split over P GPUs
+ * ("both components of our framework are highly scalable").
+ * One process per GPU, 1 <= P <= 64; every rank holds the whole CSR.  The rows are split into P
+ * contiguous ranges of equal degree-oriented slot counts; rank r scores the canonical edges of
+ * its rows ("its slice").  The caller runs three exchanges between the phases with its
+ * collective library (the binding uses torch.distributed: NCCL on a B200 node):
+ *
+ *  1. twc_dist_count(g, r, P, ws, send, send_sizes): orientation (replicated) + the triangles
+ *     whose lowest (deg, id)-key vertex is in rank r's rows, each found once (prior art
+ *     P:380).  send: device int32[2m] capacity, (oriented slot, count) pairs owed to other
+ *     ranks, grouped by destination rank in rank order; send_sizes: device int64[P], pairs per
+ *     destination (own = 0).   EXCHANGE 1: all-to-all of the pairs.
+ *  2. twc_dist_apply(g, P, ws, recv, nrecv): adds the nrecv received pairs (device
+ *     int32[2 nrecv]).
+ *  3. twc_dist_epilogue(g, r, P, deltas, k, ws, t, wedge, tw, req, req_sizes): per canonical
+ *     edge of the slice, t, wedge = d_u + d_v - 2t - 2 and TW = t - wedge (Eq. 2,
+ *     P:488-491) into t/wedge/tw (device int32[m]; only the slice is written), except the edges
+ *     whose count lives on another rank: their oriented slots go out as requests, req (device
+ *     int32[m] capacity) grouped by owner, req_sizes (device int64[P]).   EXCHANGE 2: all-to-all
+ *     of the requests; each owner answers with
+ *  4. twc_dist_serve(g, P, ws, req_in, nreq, reply): reply[i] = count of slot req_in[i]; the
+ *     replies go back with a second all-to-all (so they arrive in the order of the requests).
+ *  5. twc_dist_forest(g, P, deltas, k, ws, reply, t, wedge, tw, forest, forest_cum, kept_sizes,
+ *     nforest): completes the requested edges, filters the slice (keep iff NOT TW < delta)
+ *     and runs union-find over its kept edges threshold by threshold in descending order,
+ *     recording every hook: forest (device int32[2(n-1)] capacity) holds (a, b) pairs, those of
+ *     the i-th largest threshold before forest_cum[i] (device int64[k], cumulative); kept_sizes
+ *     (device int64[k]) = the slice's edges first kept at that threshold; nforest = total pairs.
+ *     EXCHANGE 3: all-gather of forest (padded to cap pairs), forest_cum and kept_sizes.
+ *  6. twc_dist_sweep(g, P, deltas, k, ws, forests, cap, forest_cum_all, kept_all, labels,
+ *     stats): union-find over the P forests (forests: device int32[P][2 cap]; forest_cum_all,
+ *     kept_all: device int64[P][k]; cap >= every rank's nforest) and one snapshot per
+ *     threshold: labels (device
+ *     int32[k*n]) and stats (device int64[2k] or NULL) identical to twc_sweep's on every rank.
+ * The calls of one rank must use the same g, P, deltas and workspace (it carries the oriented
+ * CSR and counts between the phases): twc_dist_workspace_bytes(n, m, rb, P).  Any output can be
+ * checked against the single-GPU calls: the union of the slices is twc_score's t, wedge, tw.
+ * Errors as elsewhere; rank / P out of range -> TWC_EINVAL.
+ * ------------------------------------------------------------------------------------- */
+size_t twc_dist_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes, int32_t world);
+twc_status twc_dist_count(const twc_csr *g, int32_t rank, int32_t world, void *workspace,
+                          size_t workspace_bytes, int32_t *send, int64_t *send_sizes,
+                          void *stream);
+twc_status twc_dist_apply(const twc_csr *g, int32_t world, void *workspace,
+                          size_t workspace_bytes, const int32_t *recv, int64_t nrecv,
+                          void *stream);
+twc_status twc_dist_epilogue(const twc_csr *g, int32_t rank, int32_t world,
+                             const double *deltas_host, int32_t k, void *workspace,
+                             size_t workspace_bytes, int32_t *t, int32_t *wedge, int32_t *tw,
+                             int32_t *req, int64_t *req_sizes, void *stream);
+twc_status twc_dist_serve(const twc_csr *g, int32_t world, void *workspace,
+                          size_t workspace_bytes, const int32_t *req, int64_t nreq,
+                          int32_t *reply, void *stream);
+twc_status twc_dist_forest(const twc_csr *g, int32_t world, const double *deltas_host, int32_t k,
+                           void *workspace, size_t workspace_bytes, const int32_t *reply,
+                           int32_t *t, int32_t *wedge, int32_t *tw, int32_t *forest,
+                           int64_t *forest_cum, int64_t *kept_sizes, int64_t *nforest,
+                           void *stream);
+twc_status twc_dist_sweep(const twc_csr *g, int32_t world, const double *deltas_host, int32_t k,
+                          void *workspace, size_t workspace_bytes, const int32_t *forests,
+                          int64_t cap, const int64_t *forest_cum_all, const int64_t *kept_all,
+                          int32_t *labels, int64_t *stats, void *stream);
+
+/* ---------------------------------------------------------------------------------------
  * twc_partition_stats -- the statistics the threshold-selection study plots for each
  * partition ("norm # CC ... norm |largest CC|", modularity P:350-352; S:346;
  * SURVEY 8(f) NEXT(2)), for k partitions of the INPUT graph g at once.

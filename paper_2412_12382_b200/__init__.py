@@ -49,11 +49,16 @@ class _Csr(ctypes.Structure):
 _lib = None
 
 
-def load_library(path: str = LIB_PATH):
-    """Load libtwc.so (raises OSError loudly when it was not built)."""
+def load_library(path: str | None = None):
+    """Load libtwc.so (raises OSError loudly when it was not built).  TWC_LIB=checked selects the
+    checked build libtwc_checked.so (device-side asserts, build.py)."""
     global _lib
     if _lib is not None:
         return _lib
+    if path is None:
+        path = LIB_PATH
+        if os.environ.get("TWC_LIB") == "checked":
+            path = os.path.join(_HERE, "libtwc_checked.so")
     if not os.path.exists(path):
         raise OSError(f"{path} not found: build it with `python -m paper_2412_12382_b200.build` "
                       "(there is no CPU fallback)")
@@ -86,6 +91,13 @@ def load_library(path: str = LIB_PATH):
         "twc_partition_stats": (ctypes.c_int, [CP, P, I32, P, SZ, P, P, P]),
         "twc_select_threshold": (ctypes.c_int, [P, P, P, I32, I64, ctypes.c_double, P, P]),
         "twc_sweep_norm_stats": (ctypes.c_int, [I64, I64, I32, P, P, P]),
+        "twc_dist_workspace_bytes": (SZ, [I64, I64, I32, I32]),
+        "twc_dist_count": (ctypes.c_int, [CP, I32, I32, P, SZ, P, P, P]),
+        "twc_dist_apply": (ctypes.c_int, [CP, I32, P, SZ, P, I64, P]),
+        "twc_dist_epilogue": (ctypes.c_int, [CP, I32, I32, P, I32, P, SZ, P, P, P, P, P, P]),
+        "twc_dist_serve": (ctypes.c_int, [CP, I32, P, SZ, P, I64, P, P]),
+        "twc_dist_forest": (ctypes.c_int, [CP, I32, P, I32, P, SZ, P, P, P, P, P, P, P, P, P]),
+        "twc_dist_sweep": (ctypes.c_int, [CP, I32, P, I32, P, SZ, P, I64, P, P, P, P, P]),
         "twc_score_shard": (ctypes.c_int, [CP, I32, I32, P, SZ, P, P]),
         "twc_finish_scores": (ctypes.c_int, [CP, P, P, SZ, P, P, P]),
     }

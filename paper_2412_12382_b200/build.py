@@ -10,8 +10,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtwc.so")
+# the checked build: the same sources with -DTWC_CHECKED, i.e. device-side asserts on every
+# shared-memory ring / staging index, every computed global index and every capacity the kernels
+# rely on (twc_common.cuh TWC_ASSERT).  compute-sanitizer is not available on this GPU pool, so
+# the test suite runs against this library instead (TWC_LIB=checked, scripts/gpu_checked.sh).
+LIB_CHECKED = os.path.join(HERE, "libtwc_checked.so")
 SOURCES = ["twc_scan.cu", "twc_score.cu", "twc_cluster.cu", "twc_similarity.cu", "twc_stats.cu",
-           "twc_k4.cu", "twc_api.cu"]
+           "twc_k4.cu", "twc_dist.cu", "twc_api.cu"]
 HEADERS = ["twc_common.cuh", "twc_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -24,26 +29,28 @@ FLAGS = [
 ]
 
 
-def _stale():
-    if not os.path.exists(LIB):
+def _stale(lib=LIB):
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "twc.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", tmp,
+def build(force=False, verbose=False, checked=False):
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not _stale(lib):
+        return lib
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [NVCC, *FLAGS, *(["-DTWC_CHECKED"] if checked else []),
+           *(["-Xptxas", "-v"] if verbose else []), "-o", tmp,
            *[os.path.join(CSRC, f) for f in SOURCES]]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv))
+    print(build(force=True, verbose="--verbose" in sys.argv, checked="--checked" in sys.argv))

@@ -519,6 +519,167 @@ twc_status twc_validate_csr(const twc_csr* g, int32_t* verdict, void* stream) {
     return TWC_OK;
 }
 
+// ---- one graph over P GPUs (twc_dist.cu) ---------------------------------------
+static constexpr int kDistMaxWorld = 64;
+
+static twc_status dist_args(const twc_csr* g, int32_t rank, int32_t world) {
+    twc_status st = check_csr(g);
+    if (st) return st;
+    if (world < 1 || world > kDistMaxWorld || rank < 0 || rank >= world)
+        return fail(TWC_EINVAL, "rank %d / world %d (1 <= world <= %d)", rank, world, kDistMaxWorld);
+    return TWC_OK;
+}
+
+static twc_status dist_thresholds(const double* deltas_host, int32_t k, long long* thr) {
+    if (k < 1 || k > 1024) return fail(TWC_EINVAL, "k=%d must be in [1, 1024]", k);
+    if (!deltas_host) return fail(TWC_EINVAL, "deltas_host is NULL");
+    for (int i = 0; i < k; ++i) {
+        twc_status st = delta_to_thr(deltas_host[i], &thr[i]);
+        if (st) return st;
+    }
+    return TWC_OK;
+}
+
+size_t twc_dist_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes, int32_t world) {
+    (void)rowptr_bytes;
+    if (n < 0 || m < 0 || world < 1 || world > kDistMaxWorld) return 0;
+    return dist_ws_bytes(n, m, world);
+}
+
+twc_status twc_dist_count(const twc_csr* g, int32_t rank, int32_t world, void* ws,
+                          size_t ws_bytes, int32_t* send, int64_t* send_sizes, void* stream) {
+    g_err.clear();
+    twc_status st = dist_args(g, rank, world);
+    if (st) return st;
+    if (!send_sizes || (g->m > 0 && !send)) return fail(TWC_EINVAL, "send buffers are NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (g->m == 0 || g->n == 0)
+        return cuda_status(cudaMemsetAsync(send_sizes, 0, sizeof(int64_t) * world, s),
+                           "twc_dist_count");
+    st = check_ws(ws, ws_bytes, dist_ws_bytes(g->n, g->m, world));
+    if (st) return st;
+    long long* sz = reinterpret_cast<long long*>(send_sizes);
+    cudaError_t e;
+    if (g->rowptr_bytes == 4)
+        e = dist_count_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx, rank,
+                                 world, ws, ws_bytes, send, sz, s);
+    else
+        e = dist_count_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr),
+                                       g->colidx, rank, world, ws, ws_bytes, send, sz, s);
+    return cuda_status(e, "twc_dist_count");
+}
+
+twc_status twc_dist_apply(const twc_csr* g, int32_t world, void* ws, size_t ws_bytes,
+                          const int32_t* recv, int64_t nrecv, void* stream) {
+    g_err.clear();
+    twc_status st = dist_args(g, 0, world);
+    if (st) return st;
+    if (nrecv < 0 || (nrecv > 0 && !recv)) return fail(TWC_EINVAL, "recv / nrecv");
+    if (g->m == 0 || g->n == 0 || nrecv == 0) return TWC_OK;
+    st = check_ws(ws, ws_bytes, dist_ws_bytes(g->n, g->m, world));
+    if (st) return st;
+    return cuda_status(dist_apply_impl(g->n, g->m, world, ws, ws_bytes, recv, nrecv,
+                                       static_cast<cudaStream_t>(stream)),
+                       "twc_dist_apply");
+}
+
+twc_status twc_dist_epilogue(const twc_csr* g, int32_t rank, int32_t world,
+                             const double* deltas_host, int32_t k, void* ws, size_t ws_bytes,
+                             int32_t* t, int32_t* wedge, int32_t* tw, int32_t* req,
+                             int64_t* req_sizes, void* stream) {
+    g_err.clear();
+    twc_status st = dist_args(g, rank, world);
+    if (st) return st;
+    long long thr[1024];
+    st = dist_thresholds(deltas_host, k, thr);
+    if (st) return st;
+    if (!req_sizes || (g->m > 0 && (!t || !wedge || !tw || !req)))
+        return fail(TWC_EINVAL, "output array is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (g->m == 0 || g->n == 0)
+        return cuda_status(cudaMemsetAsync(req_sizes, 0, sizeof(int64_t) * world, s),
+                           "twc_dist_epilogue");
+    st = check_ws(ws, ws_bytes, dist_ws_bytes(g->n, g->m, world));
+    if (st) return st;
+    long long* rs = reinterpret_cast<long long*>(req_sizes);
+    cudaError_t e;
+    if (g->rowptr_bytes == 4)
+        e = dist_epilogue_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx,
+                                    rank, world, thr, k, ws, ws_bytes, t, wedge, tw, req, rs, s);
+    else
+        e = dist_epilogue_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr),
+                                          g->colidx, rank, world, thr, k, ws, ws_bytes, t, wedge,
+                                          tw, req, rs, s);
+    return cuda_status(e, "twc_dist_epilogue");
+}
+
+twc_status twc_dist_serve(const twc_csr* g, int32_t world, void* ws, size_t ws_bytes,
+                          const int32_t* req, int64_t nreq, int32_t* reply, void* stream) {
+    g_err.clear();
+    twc_status st = dist_args(g, 0, world);
+    if (st) return st;
+    if (nreq < 0 || (nreq > 0 && (!req || !reply))) return fail(TWC_EINVAL, "req / reply");
+    if (g->m == 0 || g->n == 0 || nreq == 0) return TWC_OK;
+    st = check_ws(ws, ws_bytes, dist_ws_bytes(g->n, g->m, world));
+    if (st) return st;
+    return cuda_status(dist_serve_impl(g->n, g->m, world, ws, ws_bytes, req, nreq, reply,
+                                       static_cast<cudaStream_t>(stream)),
+                       "twc_dist_serve");
+}
+
+twc_status twc_dist_forest(const twc_csr* g, int32_t world, const double* deltas_host, int32_t k,
+                           void* ws, size_t ws_bytes, const int32_t* reply, int32_t* t,
+                           int32_t* wedge, int32_t* tw, int32_t* forest, int64_t* forest_cum,
+                           int64_t* kept_sizes, int64_t* nforest, void* stream) {
+    g_err.clear();
+    twc_status st = dist_args(g, 0, world);
+    if (st) return st;
+    long long thr[1024];
+    st = dist_thresholds(deltas_host, k, thr);
+    if (st) return st;
+    if (!forest_cum || !kept_sizes || !nforest) return fail(TWC_EINVAL, "size outputs are NULL");
+    if (g->m > 0 && g->n > 0 && (!t || !wedge || !tw || !forest))
+        return fail(TWC_EINVAL, "output array is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (g->m == 0 || g->n == 0) {
+        cudaError_t e = cudaMemsetAsync(forest_cum, 0, sizeof(int64_t) * k, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(kept_sizes, 0, sizeof(int64_t) * k, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(nforest, 0, sizeof(int64_t), s);
+        return cuda_status(e, "twc_dist_forest");
+    }
+    st = check_ws(ws, ws_bytes, dist_ws_bytes(g->n, g->m, world));
+    if (st) return st;
+    return cuda_status(
+        dist_forest_impl(g->n, g->m, world, thr, k, ws, ws_bytes, reply, t, wedge, tw, forest,
+                         reinterpret_cast<long long*>(forest_cum),
+                         reinterpret_cast<long long*>(kept_sizes),
+                         reinterpret_cast<long long*>(nforest), s),
+        "twc_dist_forest");
+}
+
+twc_status twc_dist_sweep(const twc_csr* g, int32_t world, const double* deltas_host, int32_t k,
+                          void* ws, size_t ws_bytes, const int32_t* forests, int64_t cap,
+                          const int64_t* forest_cum_all, const int64_t* kept_all,
+                          int32_t* labels, int64_t* stats, void* stream) {
+    g_err.clear();
+    twc_status st = dist_args(g, 0, world);
+    if (st) return st;
+    long long thr[1024];
+    st = dist_thresholds(deltas_host, k, thr);
+    if (st) return st;
+    if (cap < 0 || (g->n > 0 && (!labels || !forest_cum_all || !kept_all)) ||
+        (cap > 0 && !forests))
+        return fail(TWC_EINVAL, "NULL argument or cap < 0");
+    st = check_ws(ws, ws_bytes, dist_ws_bytes(g->n, g->m, world));
+    if (st) return st;
+    return cuda_status(
+        dist_sweep_impl(g->n, g->m, world, thr, k, ws, ws_bytes, forests, cap,
+                        reinterpret_cast<const long long*>(forest_cum_all),
+                        reinterpret_cast<const long long*>(kept_all), labels,
+                        reinterpret_cast<long long*>(stats), static_cast<cudaStream_t>(stream)),
+        "twc_dist_sweep");
+}
+
 // ---- K4 participation (NEXT(4)) ----------------------------------------------------------
 size_t twc_score_k4_workspace_bytes(int64_t n, int64_t m, int32_t rowptr_bytes) {
     (void)rowptr_bytes;

@@ -23,48 +23,6 @@
 
 namespace twc {
 
-__device__ __forceinline__ int uf_find(int* parent, int x) {
-    int cur = parent[x];
-    if (cur != x) {
-        int prev = x, next;
-        while (cur > (next = parent[cur])) {
-            parent[prev] = next;  // path halving; benign race, keeps parent[y] <= y
-            prev = cur;
-            cur = next;
-        }
-    }
-    return cur;
-}
-
-// Root of x, then a second walk pointing every node of the path straight at it (full
-// compression): keeps trees shallow while a band merges many components at once.
-__device__ __forceinline__ int uf_find_compress(int* parent, int x) {
-    int r = parent[x];
-    if (r == x) return r;
-    int next;
-    while (r > (next = parent[r])) r = next;
-    // Second walk, only while above r: a concurrent hook may move the path below r (r itself
-    // hooked under a smaller root), and nodes at or below r must never point at r.
-    int cur = x;
-    while (cur > r) {
-        next = parent[cur];
-        if (next > r) parent[cur] = r;  // r is an ancestor of cur and r < cur: stays a tree
-        cur = next;
-    }
-    return r;
-}
-
-__device__ __forceinline__ void uf_unite(int* parent, int u, int v) {
-    int ru = uf_find_compress(parent, u), rv = uf_find_compress(parent, v);
-    while (ru != rv) {
-        if (ru < rv) { int tmp = ru; ru = rv; rv = tmp; }  // hook the larger root ru under rv
-        const int old = atomicCAS(&parent[ru], ru, rv);
-        if (old == ru) break;
-        ru = uf_find(parent, old);
-        rv = uf_find(parent, rv);
-    }
-}
-
 __global__ void k_init_parent(int64_t n, int* __restrict__ parent) {
     int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u < n) parent[u] = (int)u;
@@ -203,6 +161,7 @@ __global__ void __launch_bounds__(256) k_hook_list(const int2* __restrict__ pair
         const unsigned j = (i * 2654435761u) & mask;
         if (j >= size) continue;
         const int2 e = pairs[beg + j];
+        TWC_ASSERT(e.x >= 0 && e.y >= 0 && e.x != e.y);
         uf_unite(parent, e.x, e.y);
     }
 }
@@ -335,6 +294,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_band_place(
             b[it] = -1;
             if (i < total) {
                 b[it] = kband[i];
+                TWC_ASSERT(b[it] >= 0 && b[it] < k);
                 r[it] = atomicAdd(&s_cnt[b[it]], 1);
             }
         }

@@ -5,6 +5,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Device-side invariant checks of the checked build (-DTWC_CHECKED, build.py): a violated
+// bound or capacity stops the kernel with an assertion naming file and line (the call then
+// returns TWC_ECUDA).  No code in the normal build.
+#ifdef TWC_CHECKED
+#include <cassert>
+#define TWC_ASSERT(x) assert(x)
+#else
+#define TWC_ASSERT(x) ((void)0)
+#endif
+
 namespace twc {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -108,6 +118,58 @@ __device__ __forceinline__ int band_of_t(V val, const T* thr, int k) {
         if (thr[mid] > (T)val) lo = mid + 1; else hi = mid;
     }
     return lo;
+}
+
+// ---- lock-free union-find (twc_cluster.cu sweep, twc_dist.cu local forests) -------------------
+// A hook always links the LARGER root under the SMALLER one with atomicCAS, so parent[x] <= x at
+// all times and the surviving root of every tree is its minimum vertex id (reading C6 / C19).
+__device__ __forceinline__ int uf_find(int* parent, int x) {
+    int cur = parent[x];
+    if (cur != x) {
+        int prev = x, next;
+        while (cur > (next = parent[cur])) {
+            parent[prev] = next;  // path halving; benign race, keeps parent[y] <= y
+            prev = cur;
+            cur = next;
+        }
+    }
+    return cur;
+}
+
+// Root of x, then a second walk pointing every node of the path straight at it (full
+// compression): keeps trees shallow while a band merges many components at once.
+__device__ __forceinline__ int uf_find_compress(int* parent, int x) {
+    int r = parent[x];
+    if (r == x) return r;
+    int next;
+    while (r > (next = parent[r])) r = next;
+    // Second walk, only while above r: a concurrent hook may move the path below r (r itself
+    // hooked under a smaller root), and nodes at or below r must never point at r.
+    int cur = x;
+    while (cur > r) {
+        next = parent[cur];
+        if (next > r) parent[cur] = r;  // r is an ancestor of cur and r < cur: stays a tree
+        cur = next;
+    }
+    return r;
+}
+
+// Unites the trees of u and v; returns true (and the hooked roots in *a <- *b, a > b) when this
+// call performed the hook, false when u and v were already connected.
+__device__ __forceinline__ bool uf_unite(int* parent, int u, int v, int* a = nullptr,
+                                         int* b = nullptr) {
+    int ru = uf_find_compress(parent, u), rv = uf_find_compress(parent, v);
+    while (ru != rv) {
+        if (ru < rv) { int tmp = ru; ru = rv; rv = tmp; }  // hook the larger root ru under rv
+        const int old = atomicCAS(&parent[ru], ru, rv);
+        if (old == ru) {
+            if (a) { *a = ru; *b = rv; }
+            return true;
+        }
+        ru = uf_find(parent, old);
+        rv = uf_find(parent, rv);
+    }
+    return false;
 }
 
 }  // namespace twc

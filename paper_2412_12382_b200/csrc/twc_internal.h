@@ -88,23 +88,103 @@ struct BinSpec {
     unsigned short* kband;  // device [m] band of kept[i]
 };
 size_t score_ws_bytes(int64_t n, int64_t m);
+
+// Epilogue of one rank of the distributed step (twc_dist.cu).
+struct DistK3 {
+    const int* cb = nullptr;  // device [world+1] canonical slice bounds
+    const int* ob = nullptr;  // device [world+1] oriented slice bounds
+    int rank = 0;
+    int4* rec = nullptr;      // device: remote edges {c, u, v, oriented slot}
+    int* nrec = nullptr;      // device counter
+};
+
+// The score workspace layout (shared with the distributed phases, twc_dist.cu, which keep the
+// oriented CSR and counts alive between their calls).
+constexpr int kSlotTile = 2048;  // K1 CSR-slot tile
+struct ScoreWs {
+    int *deg, *eoff, *rp_or, *trow, *ftrow, *tile_out, *tile_up, *opre, *upre;
+    unsigned *obits, *ubits;
+    int2* vinfo;
+    unsigned short* dslot;
+    int *col_or, *t_or, *work, *hubs, *nhubs, *range;
+};
+inline ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
+    ScoreWs w;
+    const int64_t nst = (2 * m + kSlotTile - 1) / kSlotTile;
+    const int64_t nw = (2 * m + 31) / 32;
+    w.deg = cv.take<int>(n);
+    w.eoff = cv.take<int>(n + 1);
+    w.rp_or = cv.take<int>(n + 1);
+    w.trow = cv.take<int>(num_tiles(m) + 1);
+    w.ftrow = cv.take<int>(nst + 1);
+    w.tile_out = cv.take<int>(nst);
+    w.tile_up = cv.take<int>(nst);
+    w.obits = cv.take<unsigned>(nw);
+    w.ubits = cv.take<unsigned>(nw);
+    w.opre = cv.take<int>(nw);
+    w.upre = cv.take<int>(nw);
+    w.col_or = cv.take<int>(m);
+    w.t_or = cv.take<int>(m);
+    w.vinfo = cv.take<int2>(n);
+    w.dslot = cv.take<unsigned short>(2 * m);
+    w.work = cv.take<int>(2);  // [0] K2 pivot queue, [1] K2h hub queue
+    w.hubs = cv.take<int>(n);
+    w.nhubs = cv.take<int>(1);
+    w.range = cv.take<int>(2);
+    return w;
+}
 // k4: NULL, or device int64[m] that receives the K4 participation of every canonical edge
 // (then ws must also hold k4_ws_bytes(n, m) after the score workspace)
 // shard: NULL, or {rank, world}: count only the triangles whose pivot (lowest-key vertex) lies in
 // the rank's pivot range and write only t (wedge, tw unused)
 struct ShardSpec {
     int rank, world;
+    int* bounds = nullptr;  // distributed step: device [3 (world + 1)] row / oriented / canonical
+                            // slice bounds of every rank (k_dist_bounds), else NULL
 };
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
                        cudaEvent_t* ev = nullptr, const BinSpec* bin = nullptr,
                        long long* k4 = nullptr, const ShardSpec* shard = nullptr);
+// Distributed step (twc_dist.cu): stage A = K0, K1 and K2 over this rank's pivot rows (bounds of
+// all ranks written to `bounds`); the epilogue = K3 over the rank's canonical slice (DIST mode).
+template <typename RP>
+cudaError_t dist_stage_a(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
+                         size_t ws_bytes, int rank, int world, int* bounds, cudaStream_t s);
+template <typename RP>
+cudaError_t dist_epilogue(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
+                          size_t ws_bytes, int* t, int* wedge, int* tw, const BinSpec& bin,
+                          const DistK3& d, cudaStream_t s);
 // wedge = d_u + d_v - 2t - 2, TW = 3t - d_u - d_v + 2 from canonical t (cluster workspace)
 template <typename RP>
 cudaError_t finish_scores_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
                                const int* t, void* ws, size_t ws_bytes, int* wedge, int* tw,
                                cudaStream_t s);
+
+// ---- distributed step (twc_dist.cu) ------------------------------------------------------------
+size_t dist_ws_bytes(int64_t n, int64_t m, int world);
+template <typename RP>
+cudaError_t dist_count_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, int rank,
+                            int world, void* ws, size_t ws_bytes, int* send,
+                            long long* send_sizes, cudaStream_t s);
+cudaError_t dist_apply_impl(int64_t n, int64_t m, int world, void* ws, size_t ws_bytes,
+                            const int* recv, int64_t nrecv, cudaStream_t s);
+template <typename RP>
+cudaError_t dist_epilogue_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+                               int rank, int world, const long long* thr, int k, void* ws,
+                               size_t ws_bytes, int* t, int* wedge, int* tw, int* req,
+                               long long* req_sizes, cudaStream_t s);
+cudaError_t dist_serve_impl(int64_t n, int64_t m, int world, void* ws, size_t ws_bytes,
+                            const int* req, int64_t nreq, int* reply, cudaStream_t s);
+cudaError_t dist_forest_impl(int64_t n, int64_t m, int world, const long long* thr, int k,
+                             void* ws, size_t ws_bytes, const int* reply, int* t, int* wedge,
+                             int* tw, int* forest, long long* forest_cum, long long* kept_sizes,
+                             long long* nforest, cudaStream_t s);
+cudaError_t dist_sweep_impl(int64_t n, int64_t m, int world, const long long* thr, int k,
+                            void* ws, size_t ws_bytes, const int* forests, int64_t cap,
+                            const long long* fcum_all, const long long* kept_all, int* labels,
+                            long long* stats, cudaStream_t s);
 
 // ---- K4 participation (twc_k4.cu) -----------------------------------------------------------
 int k4_big_warps();

@@ -13,6 +13,8 @@
 // count arrays, which one int32 array plus atomics avoids on a GPU.  DESIGN.md Sec. 4.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "twc_common.cuh"
@@ -43,7 +45,7 @@ __global__ void k0_degrees(int64_t n, const RP* __restrict__ rowptr, int* __rest
 // DESIGN.md Sec. 4.)
 constexpr int kSlotThreads = 256;
 constexpr int kSlotItems = 8;
-constexpr int kSlotTile = kSlotThreads * kSlotItems;  // 2048 slots
+static_assert(kSlotTile == kSlotThreads * kSlotItems, "K1 tile = 2048 slots");
 constexpr int kMaxSlotRows = 1024;
 
 // K1a: out/upper bits of every slot (8 consecutive slots per thread, one row search per
@@ -126,6 +128,7 @@ __global__ void __launch_bounds__(kSlotThreads, 8) k1_bits(
             } else {
                 ri = last_le(rowptr + r0, nr + 1, (RP)(p0 + q0));
             }
+            TWC_ASSERT(ri >= 0 && ri < nr);
             int re = rend(ri);
             int u = r0 + ri, du = rdeg(ri);
 #pragma unroll
@@ -134,6 +137,7 @@ __global__ void __launch_bounds__(kSlotThreads, 8) k1_bits(
                 if (q < tlen) {
                     while (q >= re) {  // next row (skipping empty rows)
                         ++ri;
+                        TWC_ASSERT(ri < nr);
                         re = rend(ri);
                         ++u;
                         du = rdeg(ri);
@@ -283,6 +287,7 @@ __global__ void __launch_bounds__(kSlotThreads) k1_write(
                 if ((ob >> j) & 1u) {
                     const unsigned below = (1u << j) - 1u;
                     const int sl = obase + __popc(ob & below);
+                    TWC_ASSERT(sl >= 0 && (int64_t)sl < m2 / 2);
                     col_or[sl] = v[j];
                 }
             }
@@ -358,9 +363,6 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
 // DESIGN.md Sec. 4.1 lists the variants measured on the way (ncu evidence per step).
 constexpr int kK2Warps = 8;
 constexpr int kGroupSlots = 256;
-constexpr int kFilterLog = 13;
-constexpr int kFilterBits = 1 << kFilterLog;
-constexpr int kFilterWords = kFilterBits / 32;
 constexpr int kPivotChunk = 32;
 constexpr int kQuad = 4;  // K2h: items per lane (one aligned 16-byte load)
 constexpr int kOct = 8;   // K2: items per lane (one aligned 32-byte sector, one 256-bit load)
@@ -368,9 +370,11 @@ constexpr int kRing = 128;  // candidate ring (an expansion stops before it woul
 constexpr int kRec = 64;    // record ring, >= 31 + 32 pending records
 constexpr unsigned kFiltK = 2654435761u;
 
-// 4,368 bytes per warp: 5 CTAs of 8 warps fit the 196 KB smem carveout and leave 60 KB of L1
-// for the N+(v) reads (a 228 KB carveout, i.e. 28 KB of L1, made the same kernel 18 % slower).
+// 4,368 bytes per warp at FLOG = 13: 5 CTAs of 8 warps fit the 196 KB smem carveout and leave
+// 60 KB of L1 (DESIGN.md Sec. 4.1 for the carveout / occupancy measurements).
+template <int FLOG>
 struct K2WarpSmem {
+    static constexpr int kFilterWords = (1 << FLOG) / 32;
     int list[kGroupSlots];          // staged col_or[A, B)
     unsigned filt[kFilterWords];
     int prp[33];                    // group pivot offsets rp_or[u0 .. u0+np]
@@ -380,7 +384,8 @@ struct K2WarpSmem {
     int2 rec[kRec];                 // candidate quads: {slot of the quad, mask | tag << 4}
 };
 
-__device__ __forceinline__ unsigned filter_word(unsigned x) { return x >> (32 - kFilterLog + 5); }
+template <int FLOG>
+__device__ __forceinline__ unsigned filter_word(unsigned x) { return x >> (32 - FLOG + 5); }
 
 // One aligned 32-byte sector of col_or per lane: a single 256-bit load (LDG.E.256, sm_100)
 // instead of two 128-bit loads touching the same lines twice.
@@ -397,19 +402,23 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 
 // Verify ring entries [head, head + cnt) (cnt <= 32; lane i takes entry head + i).
 // tag = (slot of u -> v) - A | pivot index << 8.
-__device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int head, int cnt, int A,
+template <typename SM>
+__device__ __forceinline__ void k2_verify(SM& S, int lane, int head, int cnt, int A,
                                           const int* __restrict__ col_or,
                                           int* __restrict__ t_or) {
     if (lane < cnt) {
         const int2 c = S.ring[(head + lane) & (kRing - 1)];
         const int sv = c.x;  // slot of v -> w
+        TWC_ASSERT(sv >= 0);
         const int w = col_or[sv];
         const int pi = c.y >> 8, so = c.y & 255;
+        TWC_ASSERT(pi >= 0 && pi < 32 && so >= 0 && so < kGroupSlots);
         const int plo = S.prp[pi] - A, len = S.prp[pi + 1] - S.prp[pi];
         const int* L = S.list + plo;
         const int q = lower_bound_bl(L, len, w);
         if (q < len && L[q] == w) {
             const int i = plo + q;
+            TWC_ASSERT(i >= 0 && i < kGroupSlots && so < kGroupSlots);
             atomicAdd(&t_or[A + i], 1);                       // t(u, w)
             atomicAdd(&t_or[A + so], 1);                      // t(u, v)
             atomicAdd(&t_or[sv], 1);                          // t(v, w)
@@ -420,8 +429,8 @@ __device__ __forceinline__ void k2_verify(K2WarpSmem& S, int lane, int head, int
 // Expand records [rhead, rhead + cnt) (cnt <= 32, lane i takes record rhead + i) into the
 // candidate ring at tail while they fit; returns the number of records consumed (a prefix; at
 // least 12 when fewer than 32 candidates are pending: a record holds at most Q = 8).
-template <int Q>
-__device__ __forceinline__ int k2_expand(K2WarpSmem& S, int lane, int rhead, int cnt, int head,
+template <int Q, typename SM>
+__device__ __forceinline__ int k2_expand(SM& S, int lane, int rhead, int cnt, int head,
                                          int& tail) {
     const int2 r = (lane < cnt) ? S.rec[(rhead + lane) & (kRec - 1)] : make_int2(0, 0);
     const unsigned cm = (unsigned)r.y & 0xffu;
@@ -442,13 +451,14 @@ __device__ __forceinline__ int k2_expand(K2WarpSmem& S, int lane, int rhead, int
     }
     const int used = __popc(fb);
     tail += __shfl_sync(FULL, incl, max(used - 1, 0)) * (used > 0);
+    TWC_ASSERT(tail - head <= kRing);
     return used;
 }
 
 // Drain: expand pending records while at least `keep` remain and verify full warps of
 // candidates.
-template <int Q>
-__device__ __forceinline__ void k2_drain(K2WarpSmem& S, int lane, int keep, int A, int& rhead,
+template <int Q, typename SM>
+__device__ __forceinline__ void k2_drain(SM& S, int lane, int keep, int A, int& rhead,
                                          int rtail, int& head, int& tail,
                                          const int* __restrict__ col_or, int* __restrict__ t_or) {
     while (rtail - rhead > keep) {
@@ -463,8 +473,8 @@ __device__ __forceinline__ void k2_drain(K2WarpSmem& S, int lane, int keep, int 
 }
 
 // range: NULL (all pivots) or device {u_lo, u_hi} of a shard (the queue starts at u_lo)
-template <int Q>
-__global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int chunk,
+template <int Q, int FLOG, int MINB>
+__global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, int chunk,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
                                                               int* __restrict__ t_or,
@@ -472,10 +482,11 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                                                               const int* __restrict__ range,
                                                               const int2* __restrict__ vinfo) {
     extern __shared__ __align__(16) unsigned char k2_smem_raw[];
-    K2WarpSmem* smem = reinterpret_cast<K2WarpSmem*>(k2_smem_raw);
+    using SM = K2WarpSmem<FLOG>;
+    SM* smem = reinterpret_cast<SM*>(k2_smem_raw);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
-    K2WarpSmem& S = smem[wid];
+    SM& S = smem[wid];
     const int64_t u_end = range ? (int64_t)range[1] : n;
     for (;;) {
         int base = 0;
@@ -496,15 +507,17 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
             }
             const int np = __popc(fit);
             const int B = __shfl_sync(FULL, e_l, np - 1);
+            TWC_ASSERT(np >= 1 && np <= 32 && B - A >= 0 && B - A <= kGroupSlots);
+            TWC_ASSERT(fit == (np == 32 ? FULL : (1u << np) - 1u));  // a prefix of the pivots
             if (lane == 0) S.prp[0] = A;
             if (lane < np) S.prp[lane + 1] = e_l;
-            for (int i = lane; i < kFilterWords; i += 32) S.filt[i] = 0u;
+            for (int i = lane; i < SM::kFilterWords; i += 32) S.filt[i] = 0u;
             __syncwarp();
             for (int i = lane; i < B - A; i += 32) {
                 const int x = __ldcs(col_or + A + i);  // read once: staged, not kept in L1
                 S.list[i] = x;
                 const unsigned h = (unsigned)x * kFiltK;
-                atomicOr(&S.filt[filter_word(h)], 1u << (h & 31));
+                atomicOr(&S.filt[filter_word<FLOG>(h)], 1u << (h & 31));
             }
             __syncwarp();
             int head = 0, tail = 0;    // candidate ring
@@ -516,10 +529,12 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                 if (s < B) {
                     const int v = S.list[s - A];
                     pi = last_le(S.prp, np + 1, s);
+                    TWC_ASSERT(pi >= 0 && pi < np && S.prp[pi] <= s && s < S.prp[pi + 1]);
                     if (S.prp[pi + 1] - S.prp[pi] >= 2) {
                         const int2 vi = vinfo[v];  // {rp_or[v], rp_or[v+1]}: one 8-byte load
                         vs = vi.x;
                         vd = vi.y - vs;
+                        TWC_ASSERT(vs >= 0 && vd >= 0 && vd < 65536);
                         // items in aligned groups of Q: [vs & ~(Q-1), vs + vd)
                         wt = (vs + vd - (vs & ~(Q - 1)) + Q - 1) / Q;
                     }
@@ -545,8 +560,10 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                     const int own = S.owner[31 - __clz(mine | 1u)];
                     // lanes past the last quad belong to the last segment and get nval <= 0
                     const int jj = mine ? own : cur;
+                    TWC_ASSERT(jj >= 0 && jj < 32);
                     const int4 sg = S.seg[jj];
                     const int sv0 = sg.x + Q * (k0 + lane);  // 4Q-byte aligned
+                    TWC_ASSERT(min(sv0, (sg.y - 1) & ~(Q - 1)) >= 0 && (sv0 & (Q - 1)) == 0);
                     // the aligned sector of this lane (clamped to the list's last group)
                     const int4* src = reinterpret_cast<const int4*>(
                         col_or + min(sv0, (sg.y - 1) & ~(Q - 1)));
@@ -566,7 +583,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                         const unsigned x = (unsigned)w[e] * kFiltK;
                         // opaque word index: keeps ptxas from folding the shift into
                         // (x >> 22) & 0x3fc + base (3 ops) so the address is SHF + LEA
-                        unsigned fw = filter_word(x);
+                        unsigned fw = filter_word<FLOG>(x);
                         asm("" : "+r"(fw));
                         const unsigned word = S.filt[fw];
                         cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
@@ -578,6 +595,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, 5) k2_intersect(int64_t n, int 
                     if (cm) S.rec[(rtail + __popc(hb & lt_mask)) & (kRec - 1)] =
                                 make_int2(sv0, (int)cm | (sg.z << 8));
                     rtail += __popc(hb);
+                    TWC_ASSERT(rtail - rhead <= kRec);
                     cur = __shfl_sync(FULL, jj, 31);
                     __syncwarp();
                     k2_drain<Q>(S, lane, 31, A, rhead, rtail, head, tail, col_or, t_or);
@@ -730,6 +748,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                     if (c) W.ring[(tail + __popc(b & lt_mask)) & (kHubRing - 1)] = cbase + e;
                     tail += __popc(b);
                 }
+                TWC_ASSERT(tail - head <= kHubRing);
                 cur = __shfl_sync(FULL, jj, 31);
                 __syncwarp();
                 while (tail - head > 0 && (tail - head >= 32 || k0 + 32 >= total)) {
@@ -742,6 +761,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                         const int* L = staged ? H.list : col_or + A;
                         const int q = staged ? lower_bound_bl(L, len, w) : lower_bound(L, len, w);
                         if (q < len && L[q] == w) {
+                            TWC_ASSERT(r0 + j - A >= 0 && r0 + j - A < len);
                             if (staged) {
                                 atomicAdd(&H.cnt[q], 1);             // t(u, w)
                                 atomicAdd(&H.cnt[r0 + j - A], 1);    // t(u, v)
@@ -786,9 +806,9 @@ __device__ __forceinline__ int sector_search(const int* __restrict__ col_or, int
     const int s_lo = ob & ~7, s_hi = (oe - 1) & ~7;
     s = max(s_lo, min(s, s_hi));
     for (;;) {
-        const int4* q = reinterpret_cast<const int4*>(col_or + s);
-        const int4 a = __ldg(q), b = __ldg(q + 1);
-        const int x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        TWC_ASSERT(s >= s_lo && s <= s_hi && s >= 0);
+        int x[8];
+        ldg_sector(col_or + s, x);  // the aligned 32-byte sector, one 256-bit load
         const int first = max(ob - s, 0), last = min(oe - s, 8) - 1;  // valid entries [first, last]
         int fv = 0, lv = 0, below = 0;
 #pragma unroll
@@ -806,7 +826,11 @@ __device__ __forceinline__ int sector_search(const int* __restrict__ col_or, int
 constexpr int kK3Threads = 256;
 constexpr int kMaxTileRows = 2048;
 
-template <typename RP, bool BIN, bool K4 = false, bool TONLY = false>
+// DIST: the epilogue of one rank of the distributed step (twc_dist.cu): only the
+// canonical edges of the rank's slice [cb[rank], cb[rank+1]); an edge whose oriented slot lies
+// outside the rank's oriented slice [ob[rank], ob[rank+1]) (a reversed edge whose far endpoint
+// belongs to another rank) is not scored here but recorded as {c, u, v, slot} for the owner.
+template <typename RP, bool BIN, bool K4 = false, bool TONLY = false, bool DIST = false>
 __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     int64_t n, int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int2* __restrict__ vinfo, const unsigned short* __restrict__ dslot,
@@ -815,7 +839,8 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     const int* __restrict__ col_or, const int* __restrict__ opre,
     const unsigned* __restrict__ obits, const int* __restrict__ t_or, int* __restrict__ t,
     int* __restrict__ wedge, int* __restrict__ tw, BinSpec bin,
-    const unsigned long long* __restrict__ k4_or = nullptr, long long* __restrict__ k4 = nullptr) {
+    const unsigned long long* __restrict__ k4_or = nullptr, long long* __restrict__ k4 = nullptr,
+    DistK3 dist = DistK3{}) {
     constexpr int kIt = kTile / kK3Threads;
     __shared__ int s_off[kMaxTileRows + 1];
     extern __shared__ __align__(8) unsigned char k3_dyn[];  // BIN: thr[k] (i64), hist[k]
@@ -830,10 +855,19 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
             s_hist[i] = 0;
         }
     }
-    const int64_t ntiles = num_tiles(m);
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int c0 = (int)(tile * kTile);
-        const int c1 = (int)min((int64_t)c0 + kTile, m);
+    int64_t tile_lo = 0, ntiles = num_tiles(m);
+    int e_lo = 0, e_hi = (int)m, o_lo = 0, o_hi = (int)m;
+    if (DIST) {
+        e_lo = dist.cb[dist.rank];
+        e_hi = dist.cb[dist.rank + 1];
+        o_lo = dist.ob[dist.rank];
+        o_hi = dist.ob[dist.rank + 1];
+        tile_lo = e_lo / kTile;
+        ntiles = num_tiles(e_hi);
+    }
+    for (int64_t tile = tile_lo + blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int c0 = max((int)(tile * kTile), e_lo);
+        const int c1 = (int)min((int64_t)tile * kTile + kTile, (int64_t)e_hi);
         const int r0 = trow[tile];
         const int nr = trow[tile + 1] - r0 + 1;  // rows touched by this tile
         const bool cached = nr <= kMaxTileRows;
@@ -846,10 +880,13 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
         unsigned kmask = 0;
 #pragma unroll
         for (int it = 0; it < kIt; ++it) {
-            const int c = c0 + it * kK3Threads + threadIdx.x;
+            const int c = (int)(tile * kTile) + it * kK3Threads + threadIdx.x;
             int bnd = -1 - lane;  // unique dummy for lanes without a kept edge
-            if (c < c1) {
+            bool remote = false;
+            int4 rrec;
+            if (c >= c0 && c < c1) {
             const int ri = cached ? last_le(s_off, nr + 1, c) : last_le(eoff + r0, nr + 1, c);
+            TWC_ASSERT(ri >= 0 && ri < nr);
             const int u = r0 + ri;
             const int eu = cached ? s_off[ri] : eoff[u];
             const int upu = (cached ? s_off[ri + 1] : eoff[u + 1]) - eu;
@@ -870,6 +907,12 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
                 const int2 vi = vinfo[v];
                 sl = sector_search(col_or, vi.x, vi.y, u, n);
             }
+            TWC_ASSERT(sl >= 0 && (int64_t)sl < m);
+            TWC_ASSERT(((ow >> (p & 31)) & 1u) || col_or[sl] == u);  // the reversed search found u
+            if (DIST && (sl < o_lo || sl >= o_hi)) {  // counted by another rank: ask its owner
+                remote = true;
+                rrec = make_int4(c, u, v, sl);
+            } else {
             const int tt = t_or[sl];
             if (K4) __stcs(k4 + c, (long long)k4_or[sl]);
             const int score = 3 * tt - du - dv + 2;
@@ -884,6 +927,16 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
                 kb[it] = bnd;
                 kmask |= 1u << it;
             }
+            }  // local edge
+            }
+            if (DIST) {  // warp-aggregated append of the remote edges
+                const unsigned rb = __ballot_sync(FULL, remote);
+                if (rb) {
+                    int base = 0;
+                    if (lane == __ffs(rb) - 1) base = atomicAdd(dist.nrec, __popc(rb));
+                    base = __shfl_sync(FULL, base, __ffs(rb) - 1);
+                    if (remote) dist.rec[base + __popc(rb & ((1u << lane) - 1u))] = rrec;
+                }
             }
             if (BIN) {  // warp-aggregated band histogram: one smem atomic per distinct band
                 const unsigned grp = __match_any_sync(FULL, bnd);
@@ -905,6 +958,7 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
             if (threadIdx.x == 0) s_base = tot ? atomicAdd(bin.nkept, tot) : 0;
             __syncthreads();
             int pos = s_base + wpre + incl - nk;
+            TWC_ASSERT(pos + nk <= m);
 #pragma unroll
             for (int it = 0; it < kIt; ++it) {
                 if ((kmask >> it) & 1u) {
@@ -923,40 +977,6 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
 }
 
 // ------------------------------------------------------------------------ host side
-struct ScoreWs {
-    int *deg, *eoff, *rp_or, *trow, *ftrow, *tile_out, *tile_up, *opre, *upre;
-    unsigned *obits, *ubits;
-    int2* vinfo;
-    unsigned short* dslot;
-    int *col_or, *t_or, *work, *hubs, *nhubs, *range;
-};
-
-static ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
-    ScoreWs w;
-    const int64_t nst = (2 * m + kSlotTile - 1) / kSlotTile;
-    const int64_t nw = (2 * m + 31) / 32;
-    w.deg = cv.take<int>(n);
-    w.eoff = cv.take<int>(n + 1);
-    w.rp_or = cv.take<int>(n + 1);
-    w.trow = cv.take<int>(num_tiles(m) + 1);
-    w.ftrow = cv.take<int>(nst + 1);
-    w.tile_out = cv.take<int>(nst);
-    w.tile_up = cv.take<int>(nst);
-    w.obits = cv.take<unsigned>(nw);
-    w.ubits = cv.take<unsigned>(nw);
-    w.opre = cv.take<int>(nw);
-    w.upre = cv.take<int>(nw);
-    w.col_or = cv.take<int>(m);
-    w.t_or = cv.take<int>(m);
-    w.vinfo = cv.take<int2>(n);
-    w.dslot = cv.take<unsigned short>(2 * m);
-    w.work = cv.take<int>(2);  // [0] K2 pivot queue, [1] K2h hub queue
-    w.hubs = cv.take<int>(n);
-    w.nhubs = cv.take<int>(1);
-    w.range = cv.take<int>(2);
-    return w;
-}
-
 size_t score_ws_bytes(int64_t n, int64_t m) {
     Carver cv(nullptr, 0);
     carve_score(cv, n, m);
@@ -997,14 +1017,66 @@ static AuxStream* aux_stream() {
     return &lanes.back();
 }
 
+// Distributed step (twc_dist.cu): the row partition of all `world` ranks, split at
+// equal oriented-slot counts: rows[r] = first u with rp_or[u] >= r m / world (rows[0] = 0,
+// rows[world] = n); the rank's oriented slice is [rp_or[rows[r]], rp_or[rows[r+1]]) and its
+// canonical slice [eoff[rows[r]], eoff[rows[r+1]]).  bounds = {rows, ob, cb}, world + 1 each.
+// Also sets this rank's K2 pivot range and points the pivot queue at it.
+__global__ void k_dist_bounds(int64_t n, int64_t m, const int* __restrict__ rp_or,
+                              const int* __restrict__ eoff, int rank, int world,
+                              int* __restrict__ bounds, int* __restrict__ range,
+                              int* __restrict__ work) {
+    const int r = threadIdx.x;
+    if (r > world) return;
+    int u;
+    if (r == 0) {
+        u = 0;
+    } else if (r == world) {
+        u = (int)n;
+    } else {
+        const int64_t target = m * r / world;
+        int64_t lo = 0, hi = n;  // first u in [0, n] with rp_or[u] >= target
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)rp_or[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        u = (int)lo;
+    }
+    bounds[r] = u;
+    bounds[world + 1 + r] = rp_or[u];
+    bounds[2 * (world + 1) + r] = eoff[u];
+    if (r == rank) {
+        range[0] = u;
+        work[0] = u;
+    }
+    if (r == rank + 1) range[1] = u;
+}
+
+// K2 variant for A/B measurements: TWC_K2="<filter log2 bits>,<min CTAs>"
+// (default 13,5), read once per process.
+typedef void (*K2Fn)(int64_t, int, const int*, const int*, int*, int*, const int*, const int2*);
+struct K2Variant {
+    K2Fn fn;
+    size_t warp_smem;
+};
+static K2Variant k2_variant() {
+    static const K2Variant v = [] {
+        int flog = 13, minb = 5;
+        if (const char* e = getenv("TWC_K2")) sscanf(e, "%d,%d", &flog, &minb);
+        if (flog == 14 && minb == 5) return K2Variant{k2_intersect<kOct, 14, 5>, sizeof(K2WarpSmem<14>)};
+        if (flog == 15) return K2Variant{k2_intersect<kOct, 15, 3>, sizeof(K2WarpSmem<15>)};
+        if (flog == 13 && minb == 6) return K2Variant{k2_intersect<kOct, 13, 6>, sizeof(K2WarpSmem<13>)};
+        return K2Variant{k2_intersect<kOct, 13, 5>, sizeof(K2WarpSmem<13>)};
+    }();
+    return v;
+}
+
+// Stage A: degrees, orientation + oriented CSR (K0, K1) and the intersection (K2h, K2) of all
+// pivots, or of a shard's pivot range.  Events [0] start, [1] orientation done, [2] K2 done.
 template <typename RP>
-cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
-                       size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
-                       cudaEvent_t* ev, const BinSpec* bin, long long* k4,
-                       const ShardSpec* shard) {
-    if (m == 0 || n == 0) return cudaGetLastError();
-    Carver cv(ws, ws_bytes);
-    ScoreWs w = carve_score(cv, n, m);
+static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+                                   const ScoreWs& w, cudaStream_t s, cudaEvent_t* ev,
+                                   const ShardSpec* shard) {
     const int sms = num_sms();
     const int64_t m2 = 2 * m;
     const int64_t nst = (m2 + kSlotTile - 1) / kSlotTile;
@@ -1030,43 +1102,58 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     cudaMemsetAsync(w.work, 0, 2 * sizeof(int), s);
     cudaMemsetAsync(w.nhubs, 0, sizeof(int), s);
     const int* range = nullptr;  // a shard counts only the triangles of its pivot range
-    if (shard && shard->world > 1) {
+    if (shard && shard->bounds) {
+        k_dist_bounds<<<1, 64 * ((shard->world + 64) / 64), 0, s>>>(
+            n, m, w.rp_or, w.eoff, shard->rank, shard->world, shard->bounds, w.range, w.work);
+        count_launches(1);
+        range = w.range;
+    } else if (shard && shard->world > 1) {
         k2_shard_range<<<1, 32, 0, s>>>(n, m, w.rp_or, shard->rank, shard->world, w.range, w.work);
         count_launches(1);
         range = w.range;
     }
     // a3: oriented intersection
-    {
-        const size_t smem = kK2Warps * sizeof(K2WarpSmem);
-        const int occ = kernel_setup((const void*)k2_intersect<kOct>, kK2Warps * 32, smem);
-        record(ev, 1, s);
-        // hub pivots (|N+(u)| > kGroupSlots, one per CTA) run on a library-owned side stream,
-        // forked from and joined back to s: they start first (the largest tasks) and the
-        // persistent K2 grid fills the SM resources they leave, so neither kernel's tail idles
-        // the GPU.  No work and an early exit when the graph has no hub.
-        AuxStream* ax = aux_stream();
-        cudaStream_t sh = ax ? ax->stream : s;
-        if (ax) {
-            cudaEventRecord(ax->fork, s);
-            cudaStreamWaitEvent(sh, ax->fork, 0);
-        }
-        k2_find_hubs<<<(unsigned)((n + 255) / 256), 256, 0, sh>>>(n, w.rp_or, w.hubs, w.nhubs,
-                                                                 range);
-        const size_t hsmem = sizeof(K2HubSmem);
-        kernel_setup((const void*)k2_hubs, kK2Warps * 32, hsmem);
-        k2_hubs<<<sms * 2, kK2Warps * 32, hsmem, sh>>>(w.rp_or, w.col_or, w.hubs, w.nhubs,
-                                                        w.work + 1, w.t_or);
-        if (ax) cudaEventRecord(ax->join, sh);
-        // pivots per queue grab: kPivotChunk, fewer when there are too few pivots to give every
-        // warp several grabs (small dense graphs), so the queue still balances the load
-        const int64_t warps = (int64_t)sms * occ * kK2Warps;
-        const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(kPivotChunk, n / (8 * warps)));
-        k2_intersect<kOct><<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or,
-                                                                   w.t_or, w.work, range, w.vinfo);
-        if (ax) cudaStreamWaitEvent(s, ax->join, 0);
-        count_launches(3);
-        record(ev, 2, s);
+    const K2Variant kv = k2_variant();
+    const size_t smem = kK2Warps * kv.warp_smem;
+    const int occ = kernel_setup((const void*)kv.fn, kK2Warps * 32, smem);
+    record(ev, 1, s);
+    // hub pivots (|N+(u)| > kGroupSlots, one per CTA) run on a library-owned side stream,
+    // forked from and joined back to s: they start first (the largest tasks) and the
+    // persistent K2 grid fills the SM resources they leave, so neither kernel's tail idles
+    // the GPU.  No work and an early exit when the graph has no hub.
+    AuxStream* ax = aux_stream();
+    cudaStream_t sh = ax ? ax->stream : s;
+    if (ax) {
+        cudaEventRecord(ax->fork, s);
+        cudaStreamWaitEvent(sh, ax->fork, 0);
     }
+    k2_find_hubs<<<(unsigned)((n + 255) / 256), 256, 0, sh>>>(n, w.rp_or, w.hubs, w.nhubs, range);
+    const size_t hsmem = sizeof(K2HubSmem);
+    kernel_setup((const void*)k2_hubs, kK2Warps * 32, hsmem);
+    k2_hubs<<<sms * 2, kK2Warps * 32, hsmem, sh>>>(w.rp_or, w.col_or, w.hubs, w.nhubs,
+                                                    w.work + 1, w.t_or);
+    if (ax) cudaEventRecord(ax->join, sh);
+    // pivots per queue grab: kPivotChunk, fewer when there are too few pivots to give every
+    // warp several grabs (small dense graphs), so the queue still balances the load
+    const int64_t warps = (int64_t)sms * occ * kK2Warps;
+    const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(kPivotChunk, n / (8 * warps)));
+    kv.fn<<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or, w.t_or, w.work,
+                                                 range, w.vinfo);
+    if (ax) cudaStreamWaitEvent(s, ax->join, 0);
+    count_launches(3);
+    record(ev, 2, s);
+}
+
+template <typename RP>
+cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
+                       size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
+                       cudaEvent_t* ev, const BinSpec* bin, long long* k4,
+                       const ShardSpec* shard) {
+    if (m == 0 || n == 0) return cudaGetLastError();
+    Carver cv(ws, ws_bytes);
+    ScoreWs w = carve_score(cv, n, m);
+    const int sms = num_sms();
+    stage_orient_intersect<RP>(n, m, rowptr, colidx, w, s, ev, shard);
     // NEXT(4): K4 participation on the same oriented CSR (workspace after the score's)
     unsigned long long* k4_or = nullptr;
     if (k4) {
@@ -1101,12 +1188,41 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     return cudaGetLastError();
 }
 
-template cudaError_t score_impl<int>(int64_t, int64_t, const int*, const int*, void*, size_t,
-                                     int*, int*, int*, cudaStream_t, cudaEvent_t*,
-                                     const BinSpec*, long long*, const ShardSpec*);
-template cudaError_t score_impl<long long>(int64_t, int64_t, const long long*, const int*,
-                                           void*, size_t, int*, int*, int*, cudaStream_t,
-                                           cudaEvent_t*, const BinSpec*, long long*,
-                                           const ShardSpec*);
+template <typename RP>
+cudaError_t dist_stage_a(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
+                         size_t ws_bytes, int rank, int world, int* bounds, cudaStream_t s) {
+    Carver cv(ws, ws_bytes);
+    ScoreWs w = carve_score(cv, n, m);
+    const ShardSpec sh{rank, world, bounds};
+    stage_orient_intersect<RP>(n, m, rowptr, colidx, w, s, nullptr, &sh);
+    return cudaGetLastError();
+}
+
+template <typename RP>
+cudaError_t dist_epilogue(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
+                          size_t ws_bytes, int* t, int* wedge, int* tw, const BinSpec& bin,
+                          const DistK3& d, cudaStream_t s) {
+    Carver cv(ws, ws_bytes);
+    ScoreWs w = carve_score(cv, n, m);
+    const int grid = grid_for(num_tiles(m), 1, num_sms() * 8);
+    k3_score<RP, true, false, false, true><<<grid, kK3Threads, (size_t)bin.k * 12, s>>>(
+        n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits,
+        w.t_or, t, wedge, tw, bin, nullptr, nullptr, d);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+#define TWC_INST(RP)                                                                            \
+    template cudaError_t score_impl<RP>(int64_t, int64_t, const RP*, const int*, void*, size_t,  \
+                                        int*, int*, int*, cudaStream_t, cudaEvent_t*,            \
+                                        const BinSpec*, long long*, const ShardSpec*);           \
+    template cudaError_t dist_stage_a<RP>(int64_t, int64_t, const RP*, const int*, void*, size_t, \
+                                          int, int, int*, cudaStream_t);                        \
+    template cudaError_t dist_epilogue<RP>(int64_t, int64_t, const RP*, const int*, void*,       \
+                                           size_t, int*, int*, int*, const BinSpec&,             \
+                                           const DistK3&, cudaStream_t);
+TWC_INST(int)
+TWC_INST(long long)
+#undef TWC_INST
 
 }  // namespace twc

@@ -68,28 +68,86 @@ def check_labels_by_properties(g, tw, delta, lab, kept, ncomp):
     assert pairs.shape[1] == ncc
 
 
+def top_pivots(g, k):
+    """The k vertices with the longest degree-oriented lists N+(u) (strict (deg, id) key, DESIGN.md
+    reading C9) -- degree bookkeeping to choose sample rows, no triangle arithmetic."""
+    rp = g.rowptr.astype(np.int64)
+    deg = np.diff(rp)
+    src = np.repeat(np.arange(g.n, dtype=np.int64), deg)
+    dst = g.colidx.astype(np.int64)
+    out = (deg[src] < deg[dst]) | ((deg[src] == deg[dst]) & (src < dst))
+    dplus = np.bincount(src[out], minlength=g.n)
+    top = np.argsort(-dplus, kind="stable")[:k]
+    return [int(u) for u in top], int(dplus[top[0]])
+
+
+def check_sampled_rows(oracle_mod, g, t, w, tw, windows):
+    s_, _ = g.canonical_pairs()
+    eoff = np.searchsorted(s_, np.arange(g.n + 1))  # first canonical id of each row
+    for u0, u1 in windows:
+        ot, ow, otw = oracle_mod.score(g, rows=(u0, u1))
+        c0, c1 = int(eoff[u0]), int(eoff[u1])
+        assert np.array_equal(t[c0:c1], ot[c0:c1]), (u0, u1)
+        assert np.array_equal(w[c0:c1], ow[c0:c1]), (u0, u1)
+        assert np.array_equal(tw[c0:c1], otw[c0:c1]), (u0, u1)
+
+
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["s-1e8"])
+@pytest.mark.parametrize("name", ["vs-1e8", "s-1e8", "d-1e8"])
 def test_rmat_1e8_sampled_parity(oracle_mod, name):
+    """P:736 / P:742 rows at 10^8 requested edges.  Sampled rows: low ids (the R-MAT hubs), the
+    rows of the 8 pivots with the longest oriented lists (d-1e8: |N+(u)| up to 854, all handled
+    by the hub kernel K2h; no R-MAT list exceeds K2h's 8,192-entry staging, see
+    test_dense_core_beyond_hub_staging), middle and high ids, a ragged end window."""
     oracle_mod.set_threads(oracle_mod.max_threads())
     g = gg.rmat_graph(name)
     rp, ci = harness.to_device(g)
     t, w, tw = twc.twc_score(rp, ci)
     torch.cuda.synchronize()
     t, w, tw = t.cpu().numpy(), w.cpu().numpy(), tw.cpu().numpy()
-    # sampled rows: low ids (the R-MAT hubs), middle and high ids, a ragged end window
-    s_, _ = g.canonical_pairs()
-    eoff = np.searchsorted(s_, np.arange(g.n + 1))  # first canonical id of each row
-    for u0, u1 in [(0, 64), (g.n // 3, g.n // 3 + 500), (g.n // 2, g.n // 2 + 2000),
-                   (g.n - 3000, g.n)]:
-        ot, ow, otw = oracle_mod.score(g, rows=(u0, u1))
-        c0, c1 = int(eoff[u0]), int(eoff[u1])
-        assert np.array_equal(t[c0:c1], ot[c0:c1]), (u0, u1)
-        assert np.array_equal(w[c0:c1], ow[c0:c1]), (u0, u1)
-        assert np.array_equal(tw[c0:c1], otw[c0:c1]), (u0, u1)
+    piv, _ = top_pivots(g, 8)
+    windows = [(0, 64), (g.n // 3, g.n // 3 + 500), (g.n // 2, g.n // 2 + 2000),
+               (g.n - 3000, g.n)] + [(u, u + 1) for u in piv]
+    check_sampled_rows(oracle_mod, g, t, w, tw, windows)
     deltas = percentile_thresholds(tw)
     twd = torch.from_numpy(tw).cuda()
     labels, stats = twc.twc_sweep(rp, ci, twd, deltas)
     lab, st = labels.cpu().numpy(), stats.cpu().numpy()
     for i, d in enumerate(deltas):
         check_labels_by_properties(g, tw, d, lab[i], int(st[i, 0]), int(st[i, 1]))
+
+
+def dense_core_graph(core, p_core, n_per, deg_per, seed):
+    """A dense core (G(core, p_core)) plus a sparse periphery attached to random core vertices:
+    every core vertex has ~p_core * core neighbours of higher (deg, id) key inside the core, so
+    the degree orientation gives pivots with |N+(u)| > 8,192 (K2h's staging) -- the global-memory
+    verification path -- on a graph with heterogeneous degrees."""
+    rng = np.random.default_rng(seed)
+    a, b = np.triu_indices(core, 1)
+    keep = rng.random(a.size) < p_core
+    a, b = a[keep], b[keep]
+    pa = np.repeat(np.arange(core, core + n_per, dtype=np.int64), deg_per)
+    pb = rng.integers(0, core + n_per, size=pa.size)
+    perm = rng.permutation(core + n_per)
+    return gg.csr_from_pairs(core + n_per, perm[np.concatenate([a, pa])],
+                             perm[np.concatenate([b, pb])], np.int64)
+
+
+@pytest.mark.slow
+def test_dense_core_beyond_hub_staging(oracle_mod):
+    oracle_mod.set_threads(oracle_mod.max_threads())
+    g = dense_core_graph(9000, 0.97, 200_000, 4, seed=21)
+    piv, dmax = top_pivots(g, 6)
+    assert dmax > 8192                       # the path under test is really reached
+    rp, ci = harness.to_device(g)
+    t, w, tw = twc.twc_score(rp, ci)
+    torch.cuda.synchronize()
+    t, w, tw = t.cpu().numpy(), w.cpu().numpy(), tw.cpu().numpy()
+    windows = [(u, u + 1) for u in piv] + [(0, 400), (g.n - 500, g.n)]
+    check_sampled_rows(oracle_mod, g, t, w, tw, windows)
+    # invariant at full size: sum t = 3 T and TW = 3t - d_u - d_v + 2 (Eq. 2 with the P:337
+    # closed form of the wedge under the a0 precondition)
+    s, d = g.canonical_pairs()
+    deg = np.diff(g.rowptr.astype(np.int64))
+    assert np.array_equal(tw.astype(np.int64), 3 * t.astype(np.int64) - deg[s] - deg[d] + 2)
+    assert int(t.astype(np.int64).sum()) % 3 == 0

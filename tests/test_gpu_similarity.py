@@ -65,7 +65,7 @@ def test_similarity_small_graphs(oracle_mod):
         check_graph(oracle_mod, g, _deltas)
 
 
-@pytest.mark.parametrize("config", [1, 2, 3])
+@pytest.mark.parametrize("config", [1, 2, 3, 4, 5])
 def test_similarity_configs(oracle_mod, config):
     check_graph(oracle_mod, gg.config_graph(config), _deltas)
 

@@ -1,11 +1,11 @@
-"""World-size-2 gloo tests of the N > 1 host logic: bench.py's replicas and max-over-ranks, and
-the exchange step of the sharded scoring path (partial counts per rank, one
-all-reduce, the sum is t).  The GPU kernels themselves are covered by tests/test_gpu_shard.py;
-here each rank's partial comes from the reference of the shard contract (tests/shard_ref.py)."""
+"""World-size-2 gloo tests of the N > 1 host logic: max-over-ranks timing and the exchanges of the
+distributed step (paper_2412_12382_b200/dist.py).  The library path itself runs in
+tests/test_gpu_dist.py (emulated ranks and two real processes on one GPU)."""
 import os
 import socket
 
 import numpy as np
+import torch
 import torch.multiprocessing as mp
 
 import graphgen as gg
@@ -57,37 +57,55 @@ def test_single_process_is_identity():
     assert harness.weak_scaling_value(100, 1, 2.0) == 50.0
 
 
-def _shard_worker(rank, world, port, q):
-    import torch
+def _comm_data(world, seed=3):
+    """Per rank: an int32 send buffer of width-2 records grouped by destination, and the record
+    counts per destination (some zero)."""
+    rng = np.random.default_rng(seed)
+    data = []
+    for r in range(world):
+        sizes = [int(x) for x in rng.integers(0, 5, size=world)]
+        sizes[r] = 0
+        buf = torch.from_numpy(rng.integers(0, 1000, size=max(2, 2 * sum(sizes))).astype(np.int32))
+        data.append((buf, sizes))
+    return data
+
+
+def _comm_worker(rank, world, port, q):
     import torch.distributed as dist
-    import paper_2412_12382_b200 as twc
-    import shard_ref
+    from paper_2412_12382_b200 import dist as tdist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    g = gg.erdos_renyi(45, 0.3, seed=5)
-    part = shard_ref.partial_counts(g, world)[rank]
-    t = torch.from_numpy(part.astype(np.int32))
-    twc.allreduce_counts(t)                      # the exchange step (NCCL on the GPU nodes)
-    q.put((rank, t.numpy().tolist(), int(part.sum())))
+    comm = tdist.TorchComm()
+    buf, sizes = _comm_data(world)[rank]
+    recv, rsz = comm.all_to_all([buf], [sizes], 2)
+    gathered = comm.all_gather([torch.tensor([rank, 10 * rank], dtype=torch.int64)])[0]
+    mx = comm.max_int([7 * rank + 1])
+    q.put((rank, recv[0][:2 * sum(rsz[0])].tolist(), rsz[0], gathered.tolist(), mx))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_two_rank_sharded_counts_gloo(oracle_mod):
-    import sys
-    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+def test_two_rank_exchanges_gloo():
+    """The three exchanges of the distributed step (paper_2412_12382_b200/dist.py TorchComm:
+    all-to-all of variable-size records, all-gather, max) over a real world-size-2 gloo group
+    equal the in-process routing the emulated GPU tests use (dist.Emulated)."""
+    from paper_2412_12382_b200 import dist as tdist
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=120) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    ot = oracle_mod.score(gg.erdos_renyi(45, 0.3, seed=5))[0]
-    for _, t, _ in res:
-        assert np.array_equal(np.array(t), ot)       # every rank holds the full t
-    assert all(r[2] > 0 for r in res)              # both ranks had triangles to count
+    data = _comm_data(world)
+    emu = tdist.Emulated(world)
+    outs, rsz = emu.all_to_all([d[0] for d in data], [d[1] for d in data], 2)
+    for r in range(world):
+        assert res[r][1] == outs[r].tolist()
+        assert res[r][2] == rsz[r]
+        assert res[r][3] == [[q_, 10 * q_] for q_ in range(world)]
+        assert res[r][4] == 7 * (world - 1) + 1
