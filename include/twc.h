@@ -195,26 +195,6 @@ twc_status twc_score_k4(const twc_csr *g, void *workspace, size_t workspace_byte
                         int32_t *wedge, int32_t *tw, int64_t *k4, void *stream);
 
 /* ---------------------------------------------------------------------------------------
- * twc_score_shard / twc_finish_scores -- the scoring step split over P GPUs.
- *
- * Every GPU holds the whole CSR.  Rank r of P (0 <= r < P) counts only the triangles whose
- * lowest (deg, id)-key vertex -- the pivot that finds each triangle exactly once (DESIGN.md
- * Sec. 4, prior art P:380) -- lies in its pivot range: the contiguous vertex range whose
- * degree-oriented lists start in [r m / P, (r+1) m / P).  The P ranges partition the vertices,
- * so summing the P partial arrays (one all-reduce of int32[m] over NCCL, the step's only
- * exchange) gives t = |N(u) & N(v)| exactly.  twc_finish_scores then derives
- *   wedge = d_u + d_v - 2t - 2  (P:337 under the simple-graph precondition)
- *   tw    = t - wedge           (Eq. 2)
- * on any rank.  t_part, t, wedge, tw: device int32[m], canonical order.  twc_score_shard
- * uses a twc_score workspace, twc_finish_scores a twc_cluster workspace.  rank outside
- * [0, P) or P < 1 -> TWC_EINVAL.  P = 1 gives t itself.
- * ------------------------------------------------------------------------------------- */
-twc_status twc_score_shard(const twc_csr *g, int32_t rank, int32_t world, void *workspace,
-                           size_t workspace_bytes, int32_t *t_part, void *stream);
-twc_status twc_finish_scores(const twc_csr *g, const int32_t *t, void *workspace,
-                             size_t workspace_bytes, int32_t *wedge, int32_t *tw, void *stream);
-
-/* ---------------------------------------------------------------------------------------
  * twc_dist_* -- the whole hot path (score + k-threshold sweep) of ONE graph split over P GPUs
  * ("both components of our framework are highly scalable").
  * One process per GPU, 1 <= P <= 64; every rank holds the whole CSR.  The rows are split into P

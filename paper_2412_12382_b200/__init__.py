@@ -98,8 +98,6 @@ def load_library(path: str | None = None):
         "twc_dist_serve": (ctypes.c_int, [CP, I32, P, SZ, P, I64, P, P]),
         "twc_dist_forest": (ctypes.c_int, [CP, I32, P, I32, P, SZ, P, P, P, P, P, P, P, P, P]),
         "twc_dist_sweep": (ctypes.c_int, [CP, I32, P, I32, P, SZ, P, I64, P, P, P, P, P]),
-        "twc_score_shard": (ctypes.c_int, [CP, I32, I32, P, SZ, P, P]),
-        "twc_finish_scores": (ctypes.c_int, [CP, P, P, SZ, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -271,55 +269,6 @@ def twc_score_sweep(rowptr, colidx, deltas, out=None, labels=None, stats=None, w
                                ws.numel(), _ptr(t), _ptr(wedge), _ptr(tw), _ptr(labels),
                                _ptr(stats), _stream(stream), ev[0] if ev else None))
     return t, wedge, tw, labels, stats
-
-
-def twc_score_shard(rowptr, colidx, rank, world, out=None, workspace=None, stream=None):
-    """Partial triangle counts of one of `world` GPUs: the triangles whose pivot
-    lies in rank's pivot range; the sum over ranks is t.  Returns device int32[m]."""
-    lib = load_library()
-    g, n, m = _graph(rowptr, colidx)
-    if out is None:
-        out = torch.empty(m, dtype=torch.int32, device=colidx.device)
-    ws = _workspace(lib.twc_score_workspace_bytes(n, m, rowptr.element_size()), colidx.device,
-                    workspace, stream)
-    _check(lib.twc_score_shard(ctypes.byref(g), int(rank), int(world), _ptr(ws), ws.numel(),
-                               _ptr(out), _stream(stream)))
-    return out
-
-
-def twc_finish_scores(rowptr, colidx, t, out=None, workspace=None, stream=None):
-    """wedge, tw (device int32[m]) from the canonical triangle counts t."""
-    lib = load_library()
-    g, n, m = _graph(rowptr, colidx)
-    dev = colidx.device
-    if out is None:
-        out = tuple(torch.empty(m, dtype=torch.int32, device=dev) for _ in range(2))
-    wedge, tw = out
-    ws = _workspace(lib.twc_cluster_workspace_bytes(n, m, rowptr.element_size()),
-                    dev, workspace, stream)
-    _check(lib.twc_finish_scores(ctypes.byref(g), _ptr(t), _ptr(ws), ws.numel(), _ptr(wedge),
-                                 _ptr(tw), _stream(stream)))
-    return wedge, tw
-
-
-def score_distributed(rowptr, colidx, group=None, workspace=None):
-    """The sharded scoring step on this process's GPU (one process per GPU, torch.distributed
-    initialised): this rank's partial counts, ONE all-reduce (sum, int32) -- NCCL over NVLink
-    on a B200 node -- then wedge and TW.  Every rank returns the full (t, wedge, tw)."""
-    import torch.distributed as dist
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    t = twc_score_shard(rowptr, colidx, rank, world, workspace=workspace)
-    allreduce_counts(t, group)
-    wedge, tw = twc_finish_scores(rowptr, colidx, t)
-    return t, wedge, tw
-
-
-def allreduce_counts(t, group=None):
-    """Sum the ranks' partial int32 counts in place (the exchange step of SURVEY 8(e))."""
-    import torch.distributed as dist
-    if dist.get_world_size(group) > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    return t
 
 
 SIM_KINDS = {"tw": 0, "tectonic": 1, "jaccard": 2, "k3": 3, "effres": 4}

@@ -323,51 +323,6 @@ twc_status twc_similarity(const twc_csr* g, const int32_t* t, int32_t kind, void
     return cuda_status(e, "twc_similarity");
 }
 
-twc_status twc_score_shard(const twc_csr* g, int32_t rank, int32_t world, void* ws,
-                           size_t ws_bytes, int32_t* t_part, void* stream) {
-    g_err.clear();
-    twc_status st = check_csr(g);
-    if (st) return st;
-    if (world < 1 || rank < 0 || rank >= world)
-        return fail(TWC_EINVAL, "rank %d / world %d", rank, world);
-    if (g->m > 0 && !t_part) return fail(TWC_EINVAL, "t_part is NULL");
-    if (g->m == 0) return TWC_OK;
-    st = check_ws(ws, ws_bytes, score_ws_bytes(g->n, g->m));
-    if (st) return st;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const ShardSpec sh{rank, world};
-    cudaError_t e;
-    if (g->rowptr_bytes == 4)
-        e = score_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx, ws,
-                            ws_bytes, t_part, nullptr, nullptr, s, nullptr, nullptr, nullptr,
-                            &sh);
-    else
-        e = score_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr),
-                                  g->colidx, ws, ws_bytes, t_part, nullptr, nullptr, s, nullptr,
-                                  nullptr, nullptr, &sh);
-    return cuda_status(e, "twc_score_shard");
-}
-
-twc_status twc_finish_scores(const twc_csr* g, const int32_t* t, void* ws, size_t ws_bytes,
-                             int32_t* wedge, int32_t* tw, void* stream) {
-    g_err.clear();
-    twc_status st = check_csr(g);
-    if (st) return st;
-    if (g->m > 0 && (!t || !wedge || !tw)) return fail(TWC_EINVAL, "t, wedge or tw is NULL");
-    if (g->m == 0) return TWC_OK;
-    st = check_ws(ws, ws_bytes, cluster_ws_bytes(g->n, g->m));
-    if (st) return st;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    cudaError_t e;
-    if (g->rowptr_bytes == 4)
-        e = finish_scores_impl<int>(g->n, g->m, static_cast<const int*>(g->rowptr), g->colidx,
-                                    t, ws, ws_bytes, wedge, tw, s);
-    else
-        e = finish_scores_impl<long long>(g->n, g->m, static_cast<const long long*>(g->rowptr),
-                                          g->colidx, t, ws, ws_bytes, wedge, tw, s);
-    return cuda_status(e, "twc_finish_scores");
-}
-
 twc_status twc_sweep_f64(const twc_csr* g, const double* score, const double* deltas_host,
                          int32_t k, void* ws, size_t ws_bytes, int32_t* labels, int64_t* stats,
                          void* stream) {

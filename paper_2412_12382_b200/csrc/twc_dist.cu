@@ -161,12 +161,14 @@ __global__ void __launch_bounds__(kDistThreads) k_foreign_write(
                 pre += (i < wid) ? s_wsum[i] : 0;
                 tot += s_wsum[i];
             }
+            const int q = nz ? owner_of(ob, world, s) : -1 - lane;  // unique dummy if none
+            const unsigned grp = __match_any_sync(FULL, q);
             if (nz) {
                 const int pos = run + pre + __popc(b & ((1u << lane) - 1u));
                 TWC_ASSERT(pos >= 0 && pos < m);
                 send[2 * pos] = s;
                 send[2 * pos + 1] = t_or[s];
-                atomicAdd(&s_hist[owner_of(ob, world, s)], 1);
+                if (lane == __ffs(grp) - 1) atomicAdd(&s_hist[q], __popc(grp));
             }
             run += tot;
         }
@@ -193,8 +195,13 @@ __global__ void k_req_hist(const int4* __restrict__ rec, const int* __restrict__
     for (int i = threadIdx.x; i < 64; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
     const int n = *nrec;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        atomicAdd(&s_hist[owner_of(ob, world, rec[i].w)], 1);
+    const int lane = threadIdx.x & 31;
+    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+        const int i = base + threadIdx.x;
+        const int q = i < n ? owner_of(ob, world, rec[i].w) : -1 - lane;
+        const unsigned grp = __match_any_sync(FULL, q);
+        if (i < n && lane == __ffs(grp) - 1) atomicAdd(&s_hist[q], __popc(grp));
+    }
     __syncthreads();
     for (int q = threadIdx.x; q < world; q += blockDim.x)
         if (s_hist[q]) atomicAdd(&hist[q], s_hist[q]);
@@ -211,16 +218,41 @@ __global__ void k_req_offsets(int world, const int* __restrict__ hist, int* __re
     }
 }
 
-__global__ void k_req_scatter(const int4* __restrict__ rec, const int* __restrict__ nrec,
-                              const int* __restrict__ ob, int world, int* __restrict__ cur,
-                              int4* __restrict__ rec_g, int* __restrict__ req) {
+// Requests grouped by owner: per chunk of blockDim records, one reservation per owner and block
+// (a handful of owners: per-record global atomics on them would serialise).
+__global__ void __launch_bounds__(kDistThreads) k_req_scatter(
+    const int4* __restrict__ rec, const int* __restrict__ nrec, const int* __restrict__ ob,
+    int world, int* __restrict__ cur, int4* __restrict__ rec_g, int* __restrict__ req) {
+    __shared__ int s_cnt[64], s_base[64];
+    const int lane = threadIdx.x & 31;
     const int n = *nrec;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int4 r = rec[i];
-        const int pos = atomicAdd(&cur[owner_of(ob, world, r.w)], 1);
-        TWC_ASSERT(pos >= 0 && pos < n);
-        rec_g[pos] = r;
-        req[pos] = r.w;
+    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+        for (int q = threadIdx.x; q < world; q += blockDim.x) s_cnt[q] = 0;
+        __syncthreads();
+        const int i = base + threadIdx.x;
+        int4 r = make_int4(0, 0, 0, 0);
+        int q = -1 - lane;
+        if (i < n) {
+            r = rec[i];
+            q = owner_of(ob, world, r.w);
+        }
+        const unsigned grp = __match_any_sync(FULL, q);
+        const int leader = __ffs(grp) - 1;
+        int wb = 0;
+        if (i < n && lane == leader) wb = atomicAdd(&s_cnt[q], __popc(grp));
+        wb = __shfl_sync(FULL, wb, leader);
+        const int rk = wb + __popc(grp & ((1u << lane) - 1u));
+        __syncthreads();
+        for (int qq = threadIdx.x; qq < world; qq += blockDim.x)
+            if (s_cnt[qq]) s_base[qq] = atomicAdd(&cur[qq], s_cnt[qq]);
+        __syncthreads();
+        if (i < n) {
+            const int pos = s_base[q] + rk;
+            TWC_ASSERT(pos >= 0 && pos < n);
+            rec_g[pos] = r;
+            req[pos] = r.w;
+        }
+        __syncthreads();
     }
 }
 
@@ -249,21 +281,35 @@ __global__ void __launch_bounds__(kDistThreads) k_finish_remote(
     }
     __syncthreads();
     const int n = *nrec;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int4 r = rec_g[i];
-        const int tt = reply[i];
-        TWC_ASSERT(tt >= 0 && r.y >= 0 && r.z > r.y);
-        const int dsum = deg[r.y] + deg[r.z];
-        const int score = 3 * tt - dsum + 2;               // Eq. 2 with the P:337 closed form
-        t[r.x] = tt;
-        wedge[r.x] = dsum - 2 * tt - 2;
-        tw[r.x] = score;
-        if ((long long)score >= s_thr[bin.k - 1]) {         // kept at the smallest threshold
-            const int b = band_of(score, s_thr, bin.k);
-            const int pos = atomicAdd(bin.nkept, 1);
-            bin.kept[pos] = make_int2(r.y, r.z);
-            bin.kband[pos] = (unsigned short)b;
-            atomicAdd(&s_hist[b], 1);
+    const int lane = threadIdx.x & 31;
+    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+        const int i = base + threadIdx.x;
+        int b = -1 - lane;  // unique dummy for lanes without a kept edge
+        int4 r = make_int4(0, 0, 0, 0);
+        if (i < n) {
+            r = rec_g[i];
+            const int tt = reply[i];
+            TWC_ASSERT(tt >= 0 && r.y >= 0 && r.z > r.y);
+            const int dsum = deg[r.y] + deg[r.z];
+            const int score = 3 * tt - dsum + 2;           // Eq. 2 with the P:337 closed form
+            t[r.x] = tt;
+            wedge[r.x] = dsum - 2 * tt - 2;
+            tw[r.x] = score;
+            if ((long long)score >= s_thr[bin.k - 1])     // kept at the smallest threshold
+                b = band_of(score, s_thr, bin.k);
+        }
+        const unsigned kb = __ballot_sync(FULL, b >= 0);
+        if (kb) {  // one reservation per warp, one smem atomic per distinct band
+            int wpos = 0;
+            if (lane == __ffs(kb) - 1) wpos = atomicAdd(bin.nkept, __popc(kb));
+            wpos = __shfl_sync(FULL, wpos, __ffs(kb) - 1);
+            const unsigned grp = __match_any_sync(FULL, b);
+            if (b >= 0) {
+                const int pos = wpos + __popc(kb & ((1u << lane) - 1u));
+                bin.kept[pos] = make_int2(r.y, r.z);
+                bin.kband[pos] = (unsigned short)b;
+                if (lane == __ffs(grp) - 1) atomicAdd(&s_hist[b], __popc(grp));
+            }
         }
     }
     __syncthreads();
@@ -278,15 +324,29 @@ __global__ void __launch_bounds__(256) k_hook_record(const int2* __restrict__ pa
                                                      int* __restrict__ forest,
                                                      int* __restrict__ fpos, int64_t cap) {
     const int beg = off[b], end = off[b + 1];
-    for (int i = beg + blockIdx.x * blockDim.x + threadIdx.x; i < end;
-         i += gridDim.x * blockDim.x) {
-        const int2 e = pairs[i];
-        int ra, rb;
-        if (uf_unite(parent, e.x, e.y, &ra, &rb)) {
-            const int pos = atomicAdd(fpos, 1);
-            TWC_ASSERT(ra > rb && rb >= 0 && pos < cap);
-            forest[2 * pos] = ra;
-            forest[2 * pos + 1] = rb;
+    const unsigned size = (unsigned)(end - beg);
+    unsigned p2 = 1;  // scrambled visiting order as k_hook_list (twc_cluster.cu)
+    while (p2 < size) p2 <<= 1;
+    const int lane = threadIdx.x & 31;
+    for (unsigned i0 = blockIdx.x * blockDim.x; i0 < p2; i0 += gridDim.x * blockDim.x) {
+        const unsigned j = ((i0 + threadIdx.x) * 2654435761u) & (p2 - 1u);
+        int ra = 0, rb = 0;
+        bool hooked = false;
+        if (i0 + threadIdx.x < p2 && j < size) {
+            const int2 e = pairs[beg + j];
+            hooked = uf_unite(parent, e.x, e.y, &ra, &rb);
+        }
+        const unsigned hb = __ballot_sync(FULL, hooked);
+        if (hb) {  // one reservation per warp
+            int wpos = 0;
+            if (lane == __ffs(hb) - 1) wpos = atomicAdd(fpos, __popc(hb));
+            wpos = __shfl_sync(FULL, wpos, __ffs(hb) - 1);
+            if (hooked) {
+                const int pos = wpos + __popc(hb & ((1u << lane) - 1u));
+                TWC_ASSERT(ra > rb && rb >= 0 && pos < cap);
+                forest[2 * pos] = ra;
+                forest[2 * pos + 1] = rb;
+            }
         }
     }
 }
@@ -410,7 +470,7 @@ cudaError_t dist_epilogue_impl(int64_t n, int64_t m, const RP* rowptr, const int
     k_req_hist<<<g, 256, 0, s>>>(w.rec, w.ctr, d.ob, world, w.ohist);
     k_req_offsets<<<1, 32, 0, s>>>(world, w.ohist, w.ocur,
                                    reinterpret_cast<unsigned long long*>(req_sizes));
-    k_req_scatter<<<g, 256, 0, s>>>(w.rec, w.ctr, d.ob, world, w.ocur, w.rec_g, req);
+    k_req_scatter<<<g, kDistThreads, 0, s>>>(w.rec, w.ctr, d.ob, world, w.ocur, w.rec_g, req);
     count_launches(3);
     return cudaGetLastError();
 }

@@ -135,18 +135,18 @@ inline ScoreWs carve_score(Carver& cv, int64_t n, int64_t m) {
 }
 // k4: NULL, or device int64[m] that receives the K4 participation of every canonical edge
 // (then ws must also hold k4_ws_bytes(n, m) after the score workspace)
-// shard: NULL, or {rank, world}: count only the triangles whose pivot (lowest-key vertex) lies in
-// the rank's pivot range and write only t (wedge, tw unused)
+// shard (the distributed step, twc_dist.cu): count only the triangles whose pivot (lowest-key
+// vertex) lies in the rank's row range; bounds: device [3 (world + 1)] row /
+// oriented / canonical slice bounds of every rank (k_dist_bounds)
 struct ShardSpec {
     int rank, world;
-    int* bounds = nullptr;  // distributed step: device [3 (world + 1)] row / oriented / canonical
-                            // slice bounds of every rank (k_dist_bounds), else NULL
+    int* bounds;
 };
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
                        cudaEvent_t* ev = nullptr, const BinSpec* bin = nullptr,
-                       long long* k4 = nullptr, const ShardSpec* shard = nullptr);
+                       long long* k4 = nullptr);
 // Distributed step (twc_dist.cu): stage A = K0, K1 and K2 over this rank's pivot rows (bounds of
 // all ranks written to `bounds`); the epilogue = K3 over the rank's canonical slice (DIST mode).
 template <typename RP>
@@ -156,12 +156,6 @@ template <typename RP>
 cudaError_t dist_epilogue(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                           size_t ws_bytes, int* t, int* wedge, int* tw, const BinSpec& bin,
                           const DistK3& d, cudaStream_t s);
-// wedge = d_u + d_v - 2t - 2, TW = 3t - d_u - d_v + 2 from canonical t (cluster workspace)
-template <typename RP>
-cudaError_t finish_scores_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
-                               const int* t, void* ws, size_t ws_bytes, int* wedge, int* tw,
-                               cudaStream_t s);
-
 // ---- distributed step (twc_dist.cu) ------------------------------------------------------------
 size_t dist_ws_bytes(int64_t n, int64_t m, int world);
 template <typename RP>

@@ -473,7 +473,10 @@ __device__ __forceinline__ void k2_drain(SM& S, int lane, int keep, int A, int& 
 }
 
 // range: NULL (all pivots) or device {u_lo, u_hi} of a shard (the queue starts at u_lo)
-template <int Q, int FLOG, int MINB>
+// GCAP < kGroupSlots: groups of at most GCAP slots (a lone pivot with more, up to kGroupSlots, is
+// a group of its own) with a 16-bits-per-slot filter of 16 GCAP bits -- at GCAP = 64 the filter
+// is 32 words, one per bank, so the warp-wide probes are conflict-free.
+template <int Q, int FLOG, int MINB, int GCAP>
 __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, int chunk,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
@@ -500,7 +503,9 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
             const int np_max = min(32, gend - u);
             const int A = rp_or[u];
             const int e_l = (lane < np_max) ? rp_or[u + lane + 1] : INT_MAX;
-            const unsigned fit = __ballot_sync(FULL, lane < np_max && e_l - A <= kGroupSlots);
+            unsigned fit = __ballot_sync(FULL, lane < np_max && e_l - A <= GCAP);
+            if (GCAP < kGroupSlots && fit == 0u && __shfl_sync(FULL, e_l, 0) - A <= kGroupSlots)
+                fit = 1u;  // a lone pivot with GCAP < |N+(u)| <= kGroupSlots
             if (fit == 0u) {  // a hub (|N+(u)| > kGroupSlots): k2_hubs takes it
                 ++u;
                 continue;
@@ -511,13 +516,18 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
             TWC_ASSERT(fit == (np == 32 ? FULL : (1u << np) - 1u));  // a prefix of the pivots
             if (lane == 0) S.prp[0] = A;
             if (lane < np) S.prp[lane + 1] = e_l;
-            for (int i = lane; i < SM::kFilterWords; i += 32) S.filt[i] = 0u;
+            // filter of this group: 2^flog bits, word = top (flog - 5) bits of the hash
+            constexpr int kSmallLog = GCAP == 64 ? 10 : GCAP == 128 ? 11 : FLOG;
+            const int fsh = (GCAP < kGroupSlots && B - A <= GCAP) ? 37 - kSmallLog : 37 - FLOG;
+            const int fwords = 1 << (32 - fsh);
+            for (int i = lane; i < fwords; i += 32) S.filt[i] = 0u;
             __syncwarp();
             for (int i = lane; i < B - A; i += 32) {
                 const int x = __ldcs(col_or + A + i);  // read once: staged, not kept in L1
                 S.list[i] = x;
                 const unsigned h = (unsigned)x * kFiltK;
-                atomicOr(&S.filt[filter_word<FLOG>(h)], 1u << (h & 31));
+                atomicOr(&S.filt[GCAP < kGroupSlots ? h >> fsh : filter_word<FLOG>(h)],
+                         1u << (h & 31));
             }
             __syncwarp();
             int head = 0, tail = 0;    // candidate ring
@@ -583,7 +593,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
                         const unsigned x = (unsigned)w[e] * kFiltK;
                         // opaque word index: keeps ptxas from folding the shift into
                         // (x >> 22) & 0x3fc + base (3 ops) so the address is SHF + LEA
-                        unsigned fw = filter_word<FLOG>(x);
+                        unsigned fw = GCAP < kGroupSlots ? x >> fsh : filter_word<FLOG>(x);
                         asm("" : "+r"(fw));
                         const unsigned word = S.filt[fw];
                         cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
@@ -608,27 +618,6 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
             u += np;
         }
     }
-}
-
-// Pivot range of a shard: rank r of P takes the pivots u whose oriented lists
-// start in [r m / P, (r+1) m / P) -- contiguous vertex ranges with equal oriented-slot counts;
-// the ranges of the P ranks partition [0, n).  Also points the pivot queue at u_lo.
-__global__ void k2_shard_range(int64_t n, int64_t m, const int* __restrict__ rp_or, int rank,
-                               int world, int* __restrict__ range, int* __restrict__ work) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    auto first_ge = [&](int64_t target) -> int {  // first u in [0, n] with rp_or[u] >= target
-        int64_t lo = 0, hi = n;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if ((int64_t)rp_or[mid] < target) lo = mid + 1; else hi = mid;
-        }
-        return (int)lo;
-    };
-    const int lo = rank == 0 ? 0 : first_ge(m * rank / world);
-    const int hi = rank == world - 1 ? (int)n : first_ge(m * (rank + 1) / world);
-    range[0] = lo;
-    range[1] = hi;
-    work[0] = lo;
 }
 
 // ------------------------------------------------------ K2h: hub pivots (|N+(u)| > 256)
@@ -830,7 +819,7 @@ constexpr int kMaxTileRows = 2048;
 // canonical edges of the rank's slice [cb[rank], cb[rank+1]); an edge whose oriented slot lies
 // outside the rank's oriented slice [ob[rank], ob[rank+1]) (a reversed edge whose far endpoint
 // belongs to another rank) is not scored here but recorded as {c, u, v, slot} for the owner.
-template <typename RP, bool BIN, bool K4 = false, bool TONLY = false, bool DIST = false>
+template <typename RP, bool BIN, bool K4 = false, bool DIST = false>
 __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     int64_t n, int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int2* __restrict__ vinfo, const unsigned short* __restrict__ dslot,
@@ -917,10 +906,8 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
             if (K4) __stcs(k4 + c, (long long)k4_or[sl]);
             const int score = 3 * tt - du - dv + 2;
             __stcs(t + c, tt);
-            if (!TONLY) {
-                __stcs(wedge + c, du + dv - 2 * tt - 2);
-                __stcs(tw + c, score);
-            }
+            __stcs(wedge + c, du + dv - 2 * tt - 2);
+            __stcs(tw + c, score);
             if (BIN && (long long)score >= s_thr[bin.k - 1]) {  // kept at the smallest threshold
                 bnd = band_of(score, s_thr, bin.k);
                 kp[it] = make_int2(u, v);
@@ -1052,8 +1039,8 @@ __global__ void k_dist_bounds(int64_t n, int64_t m, const int* __restrict__ rp_o
     if (r == rank + 1) range[1] = u;
 }
 
-// K2 variant for A/B measurements: TWC_K2="<filter log2 bits>,<min CTAs>"
-// (default 13,5), read once per process.
+// K2 variant for A/B measurements: TWC_K2="<group cap>" (64 / 128: small
+// groups with small filters; default 256), read once per process.
 typedef void (*K2Fn)(int64_t, int, const int*, const int*, int*, int*, const int*, const int2*);
 struct K2Variant {
     K2Fn fn;
@@ -1063,10 +1050,9 @@ static K2Variant k2_variant() {
     static const K2Variant v = [] {
         int flog = 13, minb = 5;
         if (const char* e = getenv("TWC_K2")) sscanf(e, "%d,%d", &flog, &minb);
-        if (flog == 14 && minb == 5) return K2Variant{k2_intersect<kOct, 14, 5>, sizeof(K2WarpSmem<14>)};
-        if (flog == 15) return K2Variant{k2_intersect<kOct, 15, 3>, sizeof(K2WarpSmem<15>)};
-        if (flog == 13 && minb == 6) return K2Variant{k2_intersect<kOct, 13, 6>, sizeof(K2WarpSmem<13>)};
-        return K2Variant{k2_intersect<kOct, 13, 5>, sizeof(K2WarpSmem<13>)};
+        if (flog == 64) return K2Variant{k2_intersect<kOct, 13, 5, 64>, sizeof(K2WarpSmem<13>)};
+        if (flog == 128) return K2Variant{k2_intersect<kOct, 13, 5, 128>, sizeof(K2WarpSmem<13>)};
+        return K2Variant{k2_intersect<kOct, 13, 5, kGroupSlots>, sizeof(K2WarpSmem<13>)};
     }();
     return v;
 }
@@ -1102,13 +1088,9 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
     cudaMemsetAsync(w.work, 0, 2 * sizeof(int), s);
     cudaMemsetAsync(w.nhubs, 0, sizeof(int), s);
     const int* range = nullptr;  // a shard counts only the triangles of its pivot range
-    if (shard && shard->bounds) {
+    if (shard) {
         k_dist_bounds<<<1, 64 * ((shard->world + 64) / 64), 0, s>>>(
             n, m, w.rp_or, w.eoff, shard->rank, shard->world, shard->bounds, w.range, w.work);
-        count_launches(1);
-        range = w.range;
-    } else if (shard && shard->world > 1) {
-        k2_shard_range<<<1, 32, 0, s>>>(n, m, w.rp_or, shard->rank, shard->world, w.range, w.work);
         count_launches(1);
         range = w.range;
     }
@@ -1147,13 +1129,12 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
 template <typename RP>
 cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx, void* ws,
                        size_t ws_bytes, int* t, int* wedge, int* tw, cudaStream_t s,
-                       cudaEvent_t* ev, const BinSpec* bin, long long* k4,
-                       const ShardSpec* shard) {
+                       cudaEvent_t* ev, const BinSpec* bin, long long* k4) {
     if (m == 0 || n == 0) return cudaGetLastError();
     Carver cv(ws, ws_bytes);
     ScoreWs w = carve_score(cv, n, m);
     const int sms = num_sms();
-    stage_orient_intersect<RP>(n, m, rowptr, colidx, w, s, ev, shard);
+    stage_orient_intersect<RP>(n, m, rowptr, colidx, w, s, ev, nullptr);
     // NEXT(4): K4 participation on the same oriented CSR (workspace after the score's)
     unsigned long long* k4_or = nullptr;
     if (k4) {
@@ -1166,11 +1147,7 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     {
         const int64_t nt = num_tiles(m);
         const int grid = grid_for(nt, 1, sms * 8);
-        if (shard)  // t only (partial counts of a shard)
-            k3_score<RP, false, false, true><<<grid, kK3Threads, 0, s>>>(
-                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre,
-                w.obits, w.t_or, t, wedge, tw, BinSpec{});
-        else if (k4)
+        if (k4)
             k3_score<RP, false, true><<<grid, kK3Threads, 0, s>>>(
                 n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre,
                 w.obits, w.t_or, t, wedge, tw, BinSpec{}, k4_or, k4);
@@ -1205,7 +1182,7 @@ cudaError_t dist_epilogue(int64_t n, int64_t m, const RP* rowptr, const int* col
     Carver cv(ws, ws_bytes);
     ScoreWs w = carve_score(cv, n, m);
     const int grid = grid_for(num_tiles(m), 1, num_sms() * 8);
-    k3_score<RP, true, false, false, true><<<grid, kK3Threads, (size_t)bin.k * 12, s>>>(
+    k3_score<RP, true, false, true><<<grid, kK3Threads, (size_t)bin.k * 12, s>>>(
         n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits,
         w.t_or, t, wedge, tw, bin, nullptr, nullptr, d);
     count_launches(1);
@@ -1215,7 +1192,7 @@ cudaError_t dist_epilogue(int64_t n, int64_t m, const RP* rowptr, const int* col
 #define TWC_INST(RP)                                                                            \
     template cudaError_t score_impl<RP>(int64_t, int64_t, const RP*, const int*, void*, size_t,  \
                                         int*, int*, int*, cudaStream_t, cudaEvent_t*,            \
-                                        const BinSpec*, long long*, const ShardSpec*);           \
+                                        const BinSpec*, long long*);                             \
     template cudaError_t dist_stage_a<RP>(int64_t, int64_t, const RP*, const int*, void*, size_t, \
                                           int, int, int*, cudaStream_t);                        \
     template cudaError_t dist_epilogue<RP>(int64_t, int64_t, const RP*, const int*, void*,       \

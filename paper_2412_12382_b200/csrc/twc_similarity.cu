@@ -79,66 +79,6 @@ cudaError_t similarity_impl(int64_t n, int64_t m, const RP* rowptr, const int* c
     return cudaGetLastError();
 }
 
-// wedge = d_u + d_v - 2t - 2 (P:337 under a0), TW = 3t - d_u - d_v + 2 (Eq. 2) from canonical
-// t, e.g. the sum over ranks of twc_score_shard's partial counts.
-template <typename RP>
-__global__ void __launch_bounds__(kSimThreads) k_finish_scores(
-    int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
-    const int* __restrict__ eoff, const int* __restrict__ trow, const int* __restrict__ t,
-    int* __restrict__ wedge, int* __restrict__ tw) {
-    __shared__ int s_off[kSimTileRows + 1];
-    const int64_t ntiles = num_tiles(m);
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int c0 = (int)(tile * kTile);
-        const int c1 = (int)min((int64_t)c0 + kTile, m);
-        const int r0 = trow[tile];
-        const int nr = trow[tile + 1] - r0 + 1;
-        const bool cached = nr <= kSimTileRows;
-        __syncthreads();
-        if (cached)
-            for (int i = threadIdx.x; i <= nr; i += blockDim.x) s_off[i] = eoff[r0 + i];
-        __syncthreads();
-        for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
-            const int ri = cached ? last_le(s_off, nr + 1, c) : last_le(eoff + r0, nr + 1, c);
-            const int u = r0 + ri;
-            const int eu = cached ? s_off[ri] : eoff[u];
-            const int upu = (cached ? s_off[ri + 1] : eoff[u + 1]) - eu;
-            const RP rb = rowptr[u];
-            const int du = (int)(rowptr[u + 1] - rb);
-            const int v = colidx[rb + (RP)(du - upu) + (RP)(c - eu)];
-            const int dv = (int)(rowptr[v + 1] - rowptr[v]);
-            const int tt = t[c];
-            wedge[c] = du + dv - 2 * tt - 2;
-            tw[c] = 3 * tt - du - dv + 2;
-        }
-    }
-}
-
-template <typename RP>
-cudaError_t finish_scores_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
-                               const int* t, void* ws, size_t ws_bytes, int* wedge, int* tw,
-                               cudaStream_t s) {
-    if (m == 0 || n == 0) return cudaGetLastError();
-    Carver cv(ws, ws_bytes);
-    int* up = cv.take<int>(n);
-    int* eoff = cv.take<int>(n + 1);
-    int* scan_tmp = cv.take<int>(scan_temp_bytes(n) / sizeof(int));
-    int* trow = cv.take<int>(num_tiles(m) + 1);
-    upper_counts<RP>(n, rowptr, colidx, up, s);
-    exclusive_scan(up, eoff, n, scan_tmp, s);
-    tile_first_rows(eoff, (int)n, m, trow, s);
-    const int grid = (int)std::min<int64_t>(num_tiles(m), (int64_t)num_sms() * 8);
-    k_finish_scores<RP><<<grid, kSimThreads, 0, s>>>(m, rowptr, colidx, eoff, trow, t, wedge, tw);
-    count_launches(1);
-    return cudaGetLastError();
-}
-
-template cudaError_t finish_scores_impl<int>(int64_t, int64_t, const int*, const int*, const int*,
-                                             void*, size_t, int*, int*, cudaStream_t);
-template cudaError_t finish_scores_impl<long long>(int64_t, int64_t, const long long*, const int*,
-                                                   const int*, void*, size_t, int*, int*,
-                                                   cudaStream_t);
-
 template cudaError_t similarity_impl<int>(int64_t, int64_t, const int*, const int*, const int*,
                                           int, void*, size_t, double*, cudaStream_t);
 template cudaError_t similarity_impl<long long>(int64_t, int64_t, const long long*, const int*,

@@ -400,18 +400,3 @@ def test_fig3_two_block_recovery(oracle_mod):
     assert rec == cond, (rec, cond)
 
 
-# ---- the reference of the sharded scoring contract (tests/shard_ref.py)
-def test_shard_reference_partitions_triangles():
-    import shard_ref
-    rng = np.random.default_rng(77)
-    for it in range(8):
-        n = int(rng.integers(3, 35))
-        g = gg.erdos_renyi(n, float(rng.uniform(0.1, 0.6)), seed=900 + it)
-        bt = brute.edge_motifs(g)
-        t = np.array([bt[k][0] for k in sorted(bt)])
-        for world in (1, 2, 3, 6):
-            ranges = shard_ref.pivot_ranges(g, world)
-            assert ranges[0][0] == 0 and ranges[-1][1] == g.n
-            assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
-            part = shard_ref.partial_counts(g, world)
-            assert np.array_equal(part.sum(axis=0), t)
