@@ -366,21 +366,22 @@ constexpr int kGroupSlots = 256;
 constexpr int kPivotChunk = 32;
 constexpr int kQuad = 4;  // K2h: items per lane (one aligned 16-byte load)
 constexpr int kOct = 8;   // K2: items per lane (one aligned 32-byte sector, one 256-bit load)
-constexpr int kRing = 128;  // candidate ring (an expansion stops before it would overflow)
+constexpr int kRing = 128;  // candidate ring, default (an expansion stops before it would overflow)
 constexpr int kRec = 64;    // record ring, >= 31 + 32 pending records
 constexpr unsigned kFiltK = 2654435761u;
 
 // 4,368 bytes per warp at FLOG = 13: 5 CTAs of 8 warps fit the 196 KB smem carveout and leave
 // 60 KB of L1 (DESIGN.md Sec. 4.1 for the carveout / occupancy measurements).
-template <int FLOG>
+template <int FLOG, int RING = kRing>
 struct K2WarpSmem {
     static constexpr int kFilterWords = (1 << FLOG) / 32;
+    static constexpr int kRingN = RING;
     int list[kGroupSlots];          // staged col_or[A, B)
     unsigned filt[kFilterWords];
     int prp[33];                    // group pivot offsets rp_or[u0 .. u0+np]
     int owner[32];                  // quad-segment owner lookup
     int4 seg[32];                   // per lane: {start of N+(v) - 4 * first quad, end, tag, 0}
-    int2 ring[kRing];               // candidates: {slot of v -> w, tag}
+    int2 ring[RING];                // candidates: {slot of v -> w, tag}
     int2 rec[kRec];                 // candidate quads: {slot of the quad, mask | tag << 4}
 };
 
@@ -396,6 +397,35 @@ __device__ __forceinline__ void ldg_sector(const int* p, int (&w)[8]) {
         : "l"(p));
 }
 
+// L2 eviction-priority hints for K3's random reads: vinfo (32 MB, each record read ~4 times) is
+// kept (evict_last), the once-read sector-search and t gathers go first (evict_first).
+__device__ __forceinline__ unsigned long long l2_policy_last() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_first() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int2 ld_v2_hint(const int2* a, unsigned long long pol) {
+    int2 r;
+    asm("ld.global.nc.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int ld_hint(const int* a, unsigned long long pol) {
+    int r;
+    asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ void ldg_sector_hint(const int* p, int (&w)[8], unsigned long long pol) {
+    asm("ld.global.nc.L2::cache_hint.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+          "=r"(w[7])
+        : "l"(p), "l"(pol));
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -407,7 +437,7 @@ __device__ __forceinline__ void k2_verify(SM& S, int lane, int head, int cnt, in
                                           const int* __restrict__ col_or,
                                           int* __restrict__ t_or) {
     if (lane < cnt) {
-        const int2 c = S.ring[(head + lane) & (kRing - 1)];
+        const int2 c = S.ring[(head + lane) & (SM::kRingN - 1)];
         const int sv = c.x;  // slot of v -> w
         TWC_ASSERT(sv >= 0);
         const int w = col_or[sv];
@@ -436,7 +466,7 @@ __device__ __forceinline__ int k2_expand(SM& S, int lane, int rhead, int cnt, in
     const unsigned cm = (unsigned)r.y & 0xffu;
     const int nc = __popc(cm);
     const int incl = warp_incl_scan(nc, lane);
-    const bool fits = lane < cnt && incl <= kRing - (tail - head);
+    const bool fits = lane < cnt && incl <= SM::kRingN - (tail - head);
     const unsigned fb = __ballot_sync(FULL, fits);
     if (fits) {
         int pos = tail + incl - nc;
@@ -444,14 +474,14 @@ __device__ __forceinline__ int k2_expand(SM& S, int lane, int rhead, int cnt, in
 #pragma unroll
         for (int e = 0; e < Q; ++e) {
             if ((cm >> e) & 1u) {
-                S.ring[pos & (kRing - 1)] = make_int2(r.x + e, tag);
+                S.ring[pos & (SM::kRingN - 1)] = make_int2(r.x + e, tag);
                 ++pos;
             }
         }
     }
     const int used = __popc(fb);
     tail += __shfl_sync(FULL, incl, max(used - 1, 0)) * (used > 0);
-    TWC_ASSERT(tail - head <= kRing);
+    TWC_ASSERT(tail - head <= SM::kRingN);
     return used;
 }
 
@@ -476,7 +506,7 @@ __device__ __forceinline__ void k2_drain(SM& S, int lane, int keep, int A, int& 
 // GCAP < kGroupSlots: groups of at most GCAP slots (a lone pivot with more, up to kGroupSlots, is
 // a group of its own) with a 16-bits-per-slot filter of 16 GCAP bits -- at GCAP = 64 the filter
 // is 32 words, one per bank, so the warp-wide probes are conflict-free.
-template <int Q, int FLOG, int MINB, int GCAP>
+template <int Q, int FLOG, int MINB, int GCAP, int RING = kRing>
 __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, int chunk,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
@@ -485,7 +515,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
                                                               const int* __restrict__ range,
                                                               const int2* __restrict__ vinfo) {
     extern __shared__ __align__(16) unsigned char k2_smem_raw[];
-    using SM = K2WarpSmem<FLOG>;
+    using SM = K2WarpSmem<FLOG, RING>;
     SM* smem = reinterpret_cast<SM*>(k2_smem_raw);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -789,7 +819,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
 // evenly over [0, n) (interpolation) and steps one sector at a time, so a typical lookup
 // touches one or two sectors instead of the log2(len) scattered sectors of a binary search.
 __device__ __forceinline__ int sector_search(const int* __restrict__ col_or, int ob, int oe, int u,
-                                             int64_t n) {
+                                             int64_t n, unsigned long long pol = 0) {
     const int len = oe - ob;
     int s = (ob + (int)(((long long)len * u) / n)) & ~7;
     const int s_lo = ob & ~7, s_hi = (oe - 1) & ~7;
@@ -797,7 +827,8 @@ __device__ __forceinline__ int sector_search(const int* __restrict__ col_or, int
     for (;;) {
         TWC_ASSERT(s >= s_lo && s <= s_hi && s >= 0);
         int x[8];
-        ldg_sector(col_or + s, x);  // the aligned 32-byte sector, one 256-bit load
+        if (pol) ldg_sector_hint(col_or + s, x, pol);
+        else ldg_sector(col_or + s, x);  // the aligned 32-byte sector, one 256-bit load
         const int first = max(ob - s, 0), last = min(oe - s, 8) - 1;  // valid entries [first, last]
         int fv = 0, lv = 0, below = 0;
 #pragma unroll
@@ -819,8 +850,9 @@ constexpr int kMaxTileRows = 2048;
 // canonical edges of the rank's slice [cb[rank], cb[rank+1]); an edge whose oriented slot lies
 // outside the rank's oriented slice [ob[rank], ob[rank+1]) (a reversed edge whose far endpoint
 // belongs to another rank) is not scored here but recorded as {c, u, v, slot} for the owner.
-template <typename RP, bool BIN, bool K4 = false, bool DIST = false>
-__global__ void __launch_bounds__(kK3Threads, 8) k3_score(
+template <typename RP, bool BIN, bool K4 = false, bool DIST = false, bool L2H = false,
+          int MINB = 8>
+__global__ void __launch_bounds__(kK3Threads, MINB) k3_score(
     int64_t n, int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int2* __restrict__ vinfo, const unsigned short* __restrict__ dslot,
     const int* __restrict__ deg, const int* __restrict__ eoff,
@@ -844,6 +876,8 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
             s_hist[i] = 0;
         }
     }
+    const unsigned long long pol_keep = L2H ? l2_policy_last() : 0ull;
+    const unsigned long long pol_once = L2H ? l2_policy_first() : 0ull;
     int64_t tile_lo = 0, ntiles = num_tiles(m);
     int e_lo = 0, e_hi = (int)m, o_lo = 0, o_hi = (int)m;
     if (DIST) {
@@ -893,8 +927,8 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
                 // aligned: oriented slot = #out-slots before p (word prefix + popc)
                 sl = opre[wi] + __popc(ow & ((1u << (p & 31)) - 1u));
             } else {  // reversed edge: u's position in N+(v), one random 8-byte record first
-                const int2 vi = vinfo[v];
-                sl = sector_search(col_or, vi.x, vi.y, u, n);
+                const int2 vi = L2H ? ld_v2_hint(vinfo + v, pol_keep) : vinfo[v];
+                sl = sector_search(col_or, vi.x, vi.y, u, n, pol_once);
             }
             TWC_ASSERT(sl >= 0 && (int64_t)sl < m);
             TWC_ASSERT(((ow >> (p & 31)) & 1u) || col_or[sl] == u);  // the reversed search found u
@@ -902,7 +936,8 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
                 remote = true;
                 rrec = make_int4(c, u, v, sl);
             } else {
-            const int tt = t_or[sl];
+            const int tt = L2H && !((ow >> (p & 31)) & 1u) ? ld_hint(t_or + sl, pol_once)
+                                                            : t_or[sl];
             if (K4) __stcs(k4 + c, (long long)k4_or[sl]);
             const int score = 3 * tt - du - dv + 2;
             __stcs(t + c, tt);
@@ -1039,20 +1074,37 @@ __global__ void k_dist_bounds(int64_t n, int64_t m, const int* __restrict__ rp_o
     if (r == rank + 1) range[1] = u;
 }
 
-// K2 variant for A/B measurements: TWC_K2="<group cap>" (64 / 128: small
-// groups with small filters; default 256), read once per process.
+// K2 variant for A/B measurements: TWC_K2="<group cap>,<filter log2 bits>,
+// <candidate ring>,<min CTAs per SM>" (default 256,13,128,5), read once per process.
 typedef void (*K2Fn)(int64_t, int, const int*, const int*, int*, int*, const int*, const int2*);
 struct K2Variant {
     K2Fn fn;
     size_t warp_smem;
+    int carveout;  // preferred smem carveout in percent (-1: the driver's choice)
 };
 static K2Variant k2_variant() {
     static const K2Variant v = [] {
-        int flog = 13, minb = 5;
-        if (const char* e = getenv("TWC_K2")) sscanf(e, "%d,%d", &flog, &minb);
-        if (flog == 64) return K2Variant{k2_intersect<kOct, 13, 5, 64>, sizeof(K2WarpSmem<13>)};
-        if (flog == 128) return K2Variant{k2_intersect<kOct, 13, 5, 128>, sizeof(K2WarpSmem<13>)};
-        return K2Variant{k2_intersect<kOct, 13, 5, kGroupSlots>, sizeof(K2WarpSmem<13>)};
+        int gcap = kGroupSlots, flog = 13, ring = kRing, minb = 5;
+        if (const char* e = getenv("TWC_K2")) sscanf(e, "%d,%d,%d,%d", &gcap, &flog, &ring, &minb);
+        if (gcap == 64) return K2Variant{k2_intersect<kOct, 13, 5, 64>, sizeof(K2WarpSmem<13>), -1};
+        if (gcap == 128) return K2Variant{k2_intersect<kOct, 13, 5, 128>, sizeof(K2WarpSmem<13>), -1};
+        // smaller candidate ring (and filter): less smem per CTA, a larger L1 for the N+(v) reads
+        if (ring == 64 && flog == 13)
+            return K2Variant{k2_intersect<kOct, 13, 5, kGroupSlots, 64>, sizeof(K2WarpSmem<13, 64>), 72};
+        if (ring == 64 && flog == 12 && minb == 6)
+            return K2Variant{k2_intersect<kOct, 12, 6, kGroupSlots, 64>, sizeof(K2WarpSmem<12, 64>), 72};
+        if (ring == 64 && flog == 12)
+            return K2Variant{k2_intersect<kOct, 12, 5, kGroupSlots, 64>, sizeof(K2WarpSmem<12, 64>), 72};
+        return K2Variant{k2_intersect<kOct, 13, 5, kGroupSlots>, sizeof(K2WarpSmem<13>), -1};
+    }();
+    return v;
+}
+
+// K3 L2 hints on/off (A/B, TWC_K3=0|1), read once per process.
+static int k3_l2_hints() {
+    static const int v = [] {
+        const char* e = getenv("TWC_K3");
+        return e ? atoi(e) : 0;
     }();
     return v;
 }
@@ -1097,6 +1149,9 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
     // a3: oriented intersection
     const K2Variant kv = k2_variant();
     const size_t smem = kK2Warps * kv.warp_smem;
+    if (kv.carveout >= 0)
+        cudaFuncSetAttribute((const void*)kv.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             kv.carveout);
     const int occ = kernel_setup((const void*)kv.fn, kK2Warps * 32, smem);
     record(ev, 1, s);
     // hub pivots (|N+(u)| > kGroupSlots, one per CTA) run on a library-owned side stream,
@@ -1151,6 +1206,18 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
             k3_score<RP, false, true><<<grid, kK3Threads, 0, s>>>(
                 n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre,
                 w.obits, w.t_or, t, wedge, tw, BinSpec{}, k4_or, k4);
+        else if (bin && k3_l2_hints() == 1)
+            k3_score<RP, true, false, false, true><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
+                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
+                wedge, tw, *bin);
+        else if (bin && k3_l2_hints() == 2)
+            k3_score<RP, true, false, false, true, 6><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
+                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
+                wedge, tw, *bin);
+        else if (bin && k3_l2_hints() == 3)
+            k3_score<RP, true, false, false, false, 6><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
+                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
+                wedge, tw, *bin);
         else if (bin)
             k3_score<RP, true><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
                 n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
