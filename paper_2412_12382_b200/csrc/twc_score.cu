@@ -13,8 +13,6 @@
 // count arrays, which one int32 array plus atomics avoids on a GPU.  DESIGN.md Sec. 4.
 #include <algorithm>
 #include <climits>
-#include <cstdio>
-#include <cstdlib>
 #include <vector>
 
 #include "twc_common.cuh"
@@ -397,35 +395,6 @@ __device__ __forceinline__ void ldg_sector(const int* p, int (&w)[8]) {
         : "l"(p));
 }
 
-// L2 eviction-priority hints for K3's random reads: vinfo (32 MB, each record read ~4 times) is
-// kept (evict_last), the once-read sector-search and t gathers go first (evict_first).
-__device__ __forceinline__ unsigned long long l2_policy_last() {
-    unsigned long long p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ unsigned long long l2_policy_first() {
-    unsigned long long p;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ int2 ld_v2_hint(const int2* a, unsigned long long pol) {
-    int2 r;
-    asm("ld.global.nc.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(a), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ int ld_hint(const int* a, unsigned long long pol) {
-    int r;
-    asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ void ldg_sector_hint(const int* p, int (&w)[8], unsigned long long pol) {
-    asm("ld.global.nc.L2::cache_hint.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
-        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
-          "=r"(w[7])
-        : "l"(p), "l"(pol));
-}
-
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -503,10 +472,7 @@ __device__ __forceinline__ void k2_drain(SM& S, int lane, int keep, int A, int& 
 }
 
 // range: NULL (all pivots) or device {u_lo, u_hi} of a shard (the queue starts at u_lo)
-// GCAP < kGroupSlots: groups of at most GCAP slots (a lone pivot with more, up to kGroupSlots, is
-// a group of its own) with a 16-bits-per-slot filter of 16 GCAP bits -- at GCAP = 64 the filter
-// is 32 words, one per bank, so the warp-wide probes are conflict-free.
-template <int Q, int FLOG, int MINB, int GCAP, int RING = kRing>
+template <int Q, int FLOG, int MINB, int RING = kRing>
 __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, int chunk,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
@@ -533,9 +499,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
             const int np_max = min(32, gend - u);
             const int A = rp_or[u];
             const int e_l = (lane < np_max) ? rp_or[u + lane + 1] : INT_MAX;
-            unsigned fit = __ballot_sync(FULL, lane < np_max && e_l - A <= GCAP);
-            if (GCAP < kGroupSlots && fit == 0u && __shfl_sync(FULL, e_l, 0) - A <= kGroupSlots)
-                fit = 1u;  // a lone pivot with GCAP < |N+(u)| <= kGroupSlots
+            const unsigned fit = __ballot_sync(FULL, lane < np_max && e_l - A <= kGroupSlots);
             if (fit == 0u) {  // a hub (|N+(u)| > kGroupSlots): k2_hubs takes it
                 ++u;
                 continue;
@@ -546,18 +510,13 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
             TWC_ASSERT(fit == (np == 32 ? FULL : (1u << np) - 1u));  // a prefix of the pivots
             if (lane == 0) S.prp[0] = A;
             if (lane < np) S.prp[lane + 1] = e_l;
-            // filter of this group: 2^flog bits, word = top (flog - 5) bits of the hash
-            constexpr int kSmallLog = GCAP == 64 ? 10 : GCAP == 128 ? 11 : FLOG;
-            const int fsh = (GCAP < kGroupSlots && B - A <= GCAP) ? 37 - kSmallLog : 37 - FLOG;
-            const int fwords = 1 << (32 - fsh);
-            for (int i = lane; i < fwords; i += 32) S.filt[i] = 0u;
+            for (int i = lane; i < SM::kFilterWords; i += 32) S.filt[i] = 0u;
             __syncwarp();
             for (int i = lane; i < B - A; i += 32) {
                 const int x = __ldcs(col_or + A + i);  // read once: staged, not kept in L1
                 S.list[i] = x;
                 const unsigned h = (unsigned)x * kFiltK;
-                atomicOr(&S.filt[GCAP < kGroupSlots ? h >> fsh : filter_word<FLOG>(h)],
-                         1u << (h & 31));
+                atomicOr(&S.filt[filter_word<FLOG>(h)], 1u << (h & 31));
             }
             __syncwarp();
             int head = 0, tail = 0;    // candidate ring
@@ -623,7 +582,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
                         const unsigned x = (unsigned)w[e] * kFiltK;
                         // opaque word index: keeps ptxas from folding the shift into
                         // (x >> 22) & 0x3fc + base (3 ops) so the address is SHF + LEA
-                        unsigned fw = GCAP < kGroupSlots ? x >> fsh : filter_word<FLOG>(x);
+                        unsigned fw = filter_word<FLOG>(x);
                         asm("" : "+r"(fw));
                         const unsigned word = S.filt[fw];
                         cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
@@ -819,7 +778,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
 // evenly over [0, n) (interpolation) and steps one sector at a time, so a typical lookup
 // touches one or two sectors instead of the log2(len) scattered sectors of a binary search.
 __device__ __forceinline__ int sector_search(const int* __restrict__ col_or, int ob, int oe, int u,
-                                             int64_t n, unsigned long long pol = 0) {
+                                             int64_t n) {
     const int len = oe - ob;
     int s = (ob + (int)(((long long)len * u) / n)) & ~7;
     const int s_lo = ob & ~7, s_hi = (oe - 1) & ~7;
@@ -827,8 +786,7 @@ __device__ __forceinline__ int sector_search(const int* __restrict__ col_or, int
     for (;;) {
         TWC_ASSERT(s >= s_lo && s <= s_hi && s >= 0);
         int x[8];
-        if (pol) ldg_sector_hint(col_or + s, x, pol);
-        else ldg_sector(col_or + s, x);  // the aligned 32-byte sector, one 256-bit load
+        ldg_sector(col_or + s, x);  // the aligned 32-byte sector, one 256-bit load
         const int first = max(ob - s, 0), last = min(oe - s, 8) - 1;  // valid entries [first, last]
         int fv = 0, lv = 0, below = 0;
 #pragma unroll
@@ -844,15 +802,16 @@ __device__ __forceinline__ int sector_search(const int* __restrict__ col_or, int
 }
 
 constexpr int kK3Threads = 256;
+// dynamic smem of a binning K3: kept edges of a tile (int2 + u16 each), thresholds, histogram
+inline size_t k3_bin_smem(int k) { return (size_t)10 * kTile + (size_t)k * 12; }
 constexpr int kMaxTileRows = 2048;
 
 // DIST: the epilogue of one rank of the distributed step (twc_dist.cu): only the
 // canonical edges of the rank's slice [cb[rank], cb[rank+1]); an edge whose oriented slot lies
 // outside the rank's oriented slice [ob[rank], ob[rank+1]) (a reversed edge whose far endpoint
 // belongs to another rank) is not scored here but recorded as {c, u, v, slot} for the owner.
-template <typename RP, bool BIN, bool K4 = false, bool DIST = false, bool L2H = false,
-          int MINB = 8>
-__global__ void __launch_bounds__(kK3Threads, MINB) k3_score(
+template <typename RP, bool BIN, bool K4 = false, bool DIST = false>
+__global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     int64_t n, int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int2* __restrict__ vinfo, const unsigned short* __restrict__ dslot,
     const int* __restrict__ deg, const int* __restrict__ eoff,
@@ -864,9 +823,14 @@ __global__ void __launch_bounds__(kK3Threads, MINB) k3_score(
     DistK3 dist = DistK3{}) {
     constexpr int kIt = kTile / kK3Threads;
     __shared__ int s_off[kMaxTileRows + 1];
-    extern __shared__ __align__(8) unsigned char k3_dyn[];  // BIN: thr[k] (i64), hist[k]
-    long long* s_thr = reinterpret_cast<long long*>(k3_dyn);
-    int* s_hist = reinterpret_cast<int*>(k3_dyn + 8 * (size_t)(BIN ? bin.k : 0));
+    // BIN: the tile's kept edges wait in smem for the tile's one reservation (registers would
+    // cost 12 per thread and make the 8-CTA launch spill); then thr[k] (i64), hist[k]
+    extern __shared__ __align__(8) unsigned char k3_dyn[];
+    int2* s_kp = reinterpret_cast<int2*>(k3_dyn);
+    unsigned short* s_kb = reinterpret_cast<unsigned short*>(k3_dyn + (BIN ? 8 * kTile : 0));
+    long long* s_thr = reinterpret_cast<long long*>(k3_dyn + (BIN ? 10 * kTile : 0));
+    int* s_hist = reinterpret_cast<int*>(k3_dyn + (BIN ? 10 * kTile : 0) +
+                                         8 * (size_t)(BIN ? bin.k : 0));
     __shared__ int s_wk[kK3Threads / 32];
     __shared__ int s_base;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -876,8 +840,6 @@ __global__ void __launch_bounds__(kK3Threads, MINB) k3_score(
             s_hist[i] = 0;
         }
     }
-    const unsigned long long pol_keep = L2H ? l2_policy_last() : 0ull;
-    const unsigned long long pol_once = L2H ? l2_policy_first() : 0ull;
     int64_t tile_lo = 0, ntiles = num_tiles(m);
     int e_lo = 0, e_hi = (int)m, o_lo = 0, o_hi = (int)m;
     if (DIST) {
@@ -898,8 +860,6 @@ __global__ void __launch_bounds__(kK3Threads, MINB) k3_score(
         if (cached)
             for (int i = threadIdx.x; i <= nr; i += blockDim.x) s_off[i] = eoff[r0 + i];
         __syncthreads();
-        int2 kp[kIt];
-        int kb[kIt];
         unsigned kmask = 0;
 #pragma unroll
         for (int it = 0; it < kIt; ++it) {
@@ -927,8 +887,8 @@ __global__ void __launch_bounds__(kK3Threads, MINB) k3_score(
                 // aligned: oriented slot = #out-slots before p (word prefix + popc)
                 sl = opre[wi] + __popc(ow & ((1u << (p & 31)) - 1u));
             } else {  // reversed edge: u's position in N+(v), one random 8-byte record first
-                const int2 vi = L2H ? ld_v2_hint(vinfo + v, pol_keep) : vinfo[v];
-                sl = sector_search(col_or, vi.x, vi.y, u, n, pol_once);
+                const int2 vi = vinfo[v];
+                sl = sector_search(col_or, vi.x, vi.y, u, n);
             }
             TWC_ASSERT(sl >= 0 && (int64_t)sl < m);
             TWC_ASSERT(((ow >> (p & 31)) & 1u) || col_or[sl] == u);  // the reversed search found u
@@ -936,8 +896,7 @@ __global__ void __launch_bounds__(kK3Threads, MINB) k3_score(
                 remote = true;
                 rrec = make_int4(c, u, v, sl);
             } else {
-            const int tt = L2H && !((ow >> (p & 31)) & 1u) ? ld_hint(t_or + sl, pol_once)
-                                                            : t_or[sl];
+            const int tt = t_or[sl];
             if (K4) __stcs(k4 + c, (long long)k4_or[sl]);
             const int score = 3 * tt - du - dv + 2;
             __stcs(t + c, tt);
@@ -945,8 +904,8 @@ __global__ void __launch_bounds__(kK3Threads, MINB) k3_score(
             __stcs(tw + c, score);
             if (BIN && (long long)score >= s_thr[bin.k - 1]) {  // kept at the smallest threshold
                 bnd = band_of(score, s_thr, bin.k);
-                kp[it] = make_int2(u, v);
-                kb[it] = bnd;
+                s_kp[it * kK3Threads + threadIdx.x] = make_int2(u, v);
+                s_kb[it * kK3Threads + threadIdx.x] = (unsigned short)bnd;
                 kmask |= 1u << it;
             }
             }  // local edge
@@ -984,8 +943,8 @@ __global__ void __launch_bounds__(kK3Threads, MINB) k3_score(
 #pragma unroll
             for (int it = 0; it < kIt; ++it) {
                 if ((kmask >> it) & 1u) {
-                    bin.kept[pos] = kp[it];
-                    bin.kband[pos] = (unsigned short)kb[it];
+                    bin.kept[pos] = s_kp[it * kK3Threads + threadIdx.x];
+                    bin.kband[pos] = s_kb[it * kK3Threads + threadIdx.x];
                     ++pos;
                 }
             }
@@ -1074,40 +1033,13 @@ __global__ void k_dist_bounds(int64_t n, int64_t m, const int* __restrict__ rp_o
     if (r == rank + 1) range[1] = u;
 }
 
-// K2 variant for A/B measurements: TWC_K2="<group cap>,<filter log2 bits>,
-// <candidate ring>,<min CTAs per SM>" (default 256,13,128,5), read once per process.
-typedef void (*K2Fn)(int64_t, int, const int*, const int*, int*, int*, const int*, const int2*);
-struct K2Variant {
-    K2Fn fn;
-    size_t warp_smem;
-    int carveout;  // preferred smem carveout in percent (-1: the driver's choice)
-};
-static K2Variant k2_variant() {
-    static const K2Variant v = [] {
-        int gcap = kGroupSlots, flog = 13, ring = kRing, minb = 5;
-        if (const char* e = getenv("TWC_K2")) sscanf(e, "%d,%d,%d,%d", &gcap, &flog, &ring, &minb);
-        if (gcap == 64) return K2Variant{k2_intersect<kOct, 13, 5, 64>, sizeof(K2WarpSmem<13>), -1};
-        if (gcap == 128) return K2Variant{k2_intersect<kOct, 13, 5, 128>, sizeof(K2WarpSmem<13>), -1};
-        // smaller candidate ring (and filter): less smem per CTA, a larger L1 for the N+(v) reads
-        if (ring == 64 && flog == 13)
-            return K2Variant{k2_intersect<kOct, 13, 5, kGroupSlots, 64>, sizeof(K2WarpSmem<13, 64>), 72};
-        if (ring == 64 && flog == 12 && minb == 6)
-            return K2Variant{k2_intersect<kOct, 12, 6, kGroupSlots, 64>, sizeof(K2WarpSmem<12, 64>), 72};
-        if (ring == 64 && flog == 12)
-            return K2Variant{k2_intersect<kOct, 12, 5, kGroupSlots, 64>, sizeof(K2WarpSmem<12, 64>), 72};
-        return K2Variant{k2_intersect<kOct, 13, 5, kGroupSlots>, sizeof(K2WarpSmem<13>), -1};
-    }();
-    return v;
-}
-
-// K3 L2 hints on/off (A/B, TWC_K3=0|1), read once per process.
-static int k3_l2_hints() {
-    static const int v = [] {
-        const char* e = getenv("TWC_K3");
-        return e ? atoi(e) : 0;
-    }();
-    return v;
-}
+// K2 launch configuration: 8,192-bit filters, a 128-entry candidate ring, 5 CTAs per SM (the
+// measured optimum; the filter / ring / group-cap / occupancy variants were
+// A/B-tested in round 2 and lost).
+constexpr int kK2FilterLog = 13;
+constexpr int kK2MinBlocks = 5;
+#define K2_KERNEL k2_intersect<kOct, kK2FilterLog, kK2MinBlocks>
+using K2Smem = K2WarpSmem<kK2FilterLog>;
 
 // Stage A: degrees, orientation + oriented CSR (K0, K1) and the intersection (K2h, K2) of all
 // pivots, or of a shard's pivot range.  Events [0] start, [1] orientation done, [2] K2 done.
@@ -1147,12 +1079,8 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
         range = w.range;
     }
     // a3: oriented intersection
-    const K2Variant kv = k2_variant();
-    const size_t smem = kK2Warps * kv.warp_smem;
-    if (kv.carveout >= 0)
-        cudaFuncSetAttribute((const void*)kv.fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             kv.carveout);
-    const int occ = kernel_setup((const void*)kv.fn, kK2Warps * 32, smem);
+    const size_t smem = kK2Warps * sizeof(K2Smem);
+    const int occ = kernel_setup((const void*)K2_KERNEL, kK2Warps * 32, smem);
     record(ev, 1, s);
     // hub pivots (|N+(u)| > kGroupSlots, one per CTA) run on a library-owned side stream,
     // forked from and joined back to s: they start first (the largest tasks) and the
@@ -1174,8 +1102,8 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
     // warp several grabs (small dense graphs), so the queue still balances the load
     const int64_t warps = (int64_t)sms * occ * kK2Warps;
     const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(kPivotChunk, n / (8 * warps)));
-    kv.fn<<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or, w.t_or, w.work,
-                                                 range, w.vinfo);
+    K2_KERNEL<<<sms * occ, kK2Warps * 32, smem, s>>>(n, chunk, w.rp_or, w.col_or, w.t_or, w.work,
+                                                     range, w.vinfo);
     if (ax) cudaStreamWaitEvent(s, ax->join, 0);
     count_launches(3);
     record(ev, 2, s);
@@ -1206,20 +1134,8 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
             k3_score<RP, false, true><<<grid, kK3Threads, 0, s>>>(
                 n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre,
                 w.obits, w.t_or, t, wedge, tw, BinSpec{}, k4_or, k4);
-        else if (bin && k3_l2_hints() == 1)
-            k3_score<RP, true, false, false, true><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
-                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
-                wedge, tw, *bin);
-        else if (bin && k3_l2_hints() == 2)
-            k3_score<RP, true, false, false, true, 6><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
-                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
-                wedge, tw, *bin);
-        else if (bin && k3_l2_hints() == 3)
-            k3_score<RP, true, false, false, false, 6><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
-                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
-                wedge, tw, *bin);
         else if (bin)
-            k3_score<RP, true><<<grid, kK3Threads, (size_t)bin->k * 12, s>>>(
+            k3_score<RP, true><<<grid, kK3Threads, k3_bin_smem(bin->k), s>>>(
                 n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
                 wedge, tw, *bin);
         else
@@ -1249,7 +1165,7 @@ cudaError_t dist_epilogue(int64_t n, int64_t m, const RP* rowptr, const int* col
     Carver cv(ws, ws_bytes);
     ScoreWs w = carve_score(cv, n, m);
     const int grid = grid_for(num_tiles(m), 1, num_sms() * 8);
-    k3_score<RP, true, false, true><<<grid, kK3Threads, (size_t)bin.k * 12, s>>>(
+    k3_score<RP, true, false, true><<<grid, kK3Threads, k3_bin_smem(bin.k), s>>>(
         n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits,
         w.t_or, t, wedge, tw, bin, nullptr, nullptr, d);
     count_launches(1);
