@@ -442,13 +442,12 @@ cudaError_t score_sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* 
     sweep_upload(P, w.thr, w.order, s);
     cudaMemsetAsync(w.cnt, 0, sizeof(int) * (k + 1), s);
     cudaMemsetAsync(w.nkept, 0, sizeof(int), s);
-    BinSpec bin{w.thr, k, w.cnt, w.nkept, w.kept, w.kband};
+    BinSpec bin{w.thr, k, w.cnt, w.nkept, w.kept, w.kband, w.parent};  // K0 initialises parent
     cudaError_t e = score_impl<RP>(n, m, rowptr, colidx, w.score, w.score_bytes, t, wedge, tw, s,
                                    ev, &bin);
     if (e != cudaSuccess) return e;
     band_offsets(w.cnt, k, w.order, w.off, w.cursor, st, s);
     band_place(w.kept, w.kband, w.nkept, m, k, w.cursor, w.pairs, s);
-    init_parent(n, w.parent, s);
     record(ev, 4, s);
     sweep_loop(n, m, P, w.pairs, w.off, w.parent, labels, st, s, step_ev);
     record(ev, 5, s);

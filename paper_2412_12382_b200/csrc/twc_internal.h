@@ -86,6 +86,7 @@ struct BinSpec {
     int* nkept;             // device counter (zeroed by the caller)
     int2* kept;             // device [m] (u, v) of kept edges, in no particular order
     unsigned short* kband;  // device [m] band of kept[i]
+    int* parent = nullptr;  // device [n] or NULL: union-find parents, initialised by K0 (parent[u] = u)
 };
 size_t score_ws_bytes(int64_t n, int64_t m);
 

@@ -21,10 +21,15 @@
 namespace twc {
 
 // ------------------------------------------------------------------------------ K0 degrees
+// (+ the sweep's union-find initialisation parent[u] = u when the fused call passes `parent`)
 template <typename RP>
-__global__ void k0_degrees(int64_t n, const RP* __restrict__ rowptr, int* __restrict__ deg) {
+__global__ void k0_degrees(int64_t n, const RP* __restrict__ rowptr, int* __restrict__ deg,
+                           int* __restrict__ parent) {
     int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u < n) deg[u] = (int)(rowptr[u + 1] - rowptr[u]);
+    if (u < n) {
+        deg[u] = (int)(rowptr[u + 1] - rowptr[u]);
+        if (parent) parent[u] = (int)u;
+    }
 }
 
 // ------------------------------------------------ K1: orientation over full-CSR slot tiles
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(kSlotThreads) k1_write(
     int64_t m2, const int* __restrict__ colidx, const unsigned* __restrict__ obits,
     const unsigned* __restrict__ ubits, const int* __restrict__ tile_out,
     const int* __restrict__ tile_up, int* __restrict__ opre, int* __restrict__ upre,
-    int* __restrict__ col_or) {
+    int* __restrict__ col_or, int* __restrict__ t_or) {
     __shared__ unsigned s_wsum[kSlotThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t ntiles = (m2 + kSlotTile - 1) / kSlotTile;
@@ -287,6 +292,7 @@ __global__ void __launch_bounds__(kSlotThreads) k1_write(
                     const int sl = obase + __popc(ob & below);
                     TWC_ASSERT(sl >= 0 && (int64_t)sl < m2 / 2);
                     col_or[sl] = v[j];
+                    t_or[sl] = 0;  // K2's counters start at zero (no separate memset pass)
                 }
             }
         }
@@ -1046,13 +1052,13 @@ using K2Smem = K2WarpSmem<kK2FilterLog>;
 template <typename RP>
 static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
                                    const ScoreWs& w, cudaStream_t s, cudaEvent_t* ev,
-                                   const ShardSpec* shard) {
+                                   const ShardSpec* shard, int* parent = nullptr) {
     const int sms = num_sms();
     const int64_t m2 = 2 * m;
     const int64_t nst = (m2 + kSlotTile - 1) / kSlotTile;
     record(ev, 0, s);
     // a1 + a2: degrees, orientation, oriented CSR (bits + tile counts, tile scan, scatter, rows)
-    k0_degrees<RP><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rowptr, w.deg);
+    k0_degrees<RP><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rowptr, w.deg, parent);
     count_launches(1);
     tile_rows<RP>(rowptr, (int)n, m2, kSlotTile, w.ftrow, s);
     {
@@ -1061,14 +1067,13 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
                                                  w.ubits, w.tile_out, w.tile_up, w.dslot);
         k1_tile_scan<<<1, 1024, 0, s>>>(nst, w.tile_out, w.tile_up);
         k1_write<<<grid, kSlotThreads, 0, s>>>(m2, colidx, w.obits, w.ubits, w.tile_out,
-                                               w.tile_up, w.opre, w.upre, w.col_or);
+                                               w.tile_up, w.opre, w.upre, w.col_or, w.t_or);
         k1_rows<RP><<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, m, rowptr, w.obits, w.ubits,
                                                                    w.opre, w.upre, w.rp_or, w.eoff,
                                                                    w.vinfo);
         count_launches(4);
     }
     tile_first_rows(w.eoff, (int)n, m, w.trow, s);
-    cudaMemsetAsync(w.t_or, 0, sizeof(int) * (size_t)m, s);
     cudaMemsetAsync(w.work, 0, 2 * sizeof(int), s);
     cudaMemsetAsync(w.nhubs, 0, sizeof(int), s);
     const int* range = nullptr;  // a shard counts only the triangles of its pivot range
@@ -1117,7 +1122,7 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     Carver cv(ws, ws_bytes);
     ScoreWs w = carve_score(cv, n, m);
     const int sms = num_sms();
-    stage_orient_intersect<RP>(n, m, rowptr, colidx, w, s, ev, nullptr);
+    stage_orient_intersect<RP>(n, m, rowptr, colidx, w, s, ev, nullptr, bin ? bin->parent : nullptr);
     // NEXT(4): K4 participation on the same oriented CSR (workspace after the score's)
     unsigned long long* k4_or = nullptr;
     if (k4) {
