@@ -20,10 +20,18 @@ constexpr int kSimThreads = 256;
 constexpr int kSimTileRows = 2048;
 
 template <typename RP>
+__global__ void k_sim_degrees(int64_t n, const RP* __restrict__ rowptr, int* __restrict__ deg) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n) deg[u] = (int)(rowptr[u + 1] - rowptr[u]);
+}
+
+// The far endpoint's degree comes from a 4-byte deg[] (16 MB for config 5, L2-resident) rather
+// than from two 8-byte rowptr reads of a 32 MB array: one random L2 sector per edge.
+template <typename RP>
 __global__ void __launch_bounds__(kSimThreads) k_similarity(
     int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
-    const int* __restrict__ eoff, const int* __restrict__ trow, const int* __restrict__ t,
-    int kind, double* __restrict__ out) {
+    const int* __restrict__ eoff, const int* __restrict__ trow, const int* __restrict__ deg,
+    const int* __restrict__ t, int kind, double* __restrict__ out) {
     __shared__ int s_off[kSimTileRows + 1];
     const int64_t ntiles = num_tiles(m);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -44,7 +52,7 @@ __global__ void __launch_bounds__(kSimThreads) k_similarity(
             const RP rb = rowptr[u];
             const long long du = (long long)(rowptr[u + 1] - rb);
             const int v = colidx[rb + (RP)(du - upu) + (RP)(c - eu)];
-            const long long dv = (long long)(rowptr[v + 1] - rowptr[v]);
+            const long long dv = (long long)deg[v];
             const long long tt = t[c];
             double x;
             switch (kind) {
@@ -70,12 +78,15 @@ cudaError_t similarity_impl(int64_t n, int64_t m, const RP* rowptr, const int* c
     int* eoff = cv.take<int>(n + 1);
     int* scan_tmp = cv.take<int>(scan_temp_bytes(n) / sizeof(int));
     int* trow = cv.take<int>(num_tiles(m) + 1);
+    int* deg = cv.take<int>(n);
     upper_counts<RP>(n, rowptr, colidx, up, s);
     exclusive_scan(up, eoff, n, scan_tmp, s);
     tile_first_rows(eoff, (int)n, m, trow, s);
+    k_sim_degrees<RP><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rowptr, deg);
     const int grid = (int)std::min<int64_t>(num_tiles(m), (int64_t)num_sms() * 8);
-    k_similarity<RP><<<grid, kSimThreads, 0, s>>>(m, rowptr, colidx, eoff, trow, t, kind, out);
-    count_launches(1);
+    k_similarity<RP><<<grid, kSimThreads, 0, s>>>(m, rowptr, colidx, eoff, trow, deg, t, kind,
+                                                  out);
+    count_launches(2);
     return cudaGetLastError();
 }
 
