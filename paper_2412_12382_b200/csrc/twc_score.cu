@@ -1046,6 +1046,7 @@ constexpr int kK2MinBlocks = 5;
 #define K2_KERNEL k2_intersect<kOct, kK2FilterLog, kK2MinBlocks>
 using K2Smem = K2WarpSmem<kK2FilterLog>;
 
+
 // Stage A: degrees, orientation + oriented CSR (K0, K1) and the intersection (K2h, K2) of all
 // pivots, or of a shard's pivot range.  Events [0] start, [1] orientation done, [2] K2 done.
 template <typename RP>
