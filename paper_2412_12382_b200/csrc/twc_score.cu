@@ -367,7 +367,6 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
 constexpr int kK2Warps = 8;
 constexpr int kGroupSlots = 256;
 constexpr int kPivotChunk = 32;
-constexpr int kQuad = 4;  // K2h: items per lane (one aligned 16-byte load)
 constexpr int kOct = 8;   // K2: items per lane (one aligned 32-byte sector, one 256-bit load)
 constexpr int kRing = 128;  // candidate ring, default (an expansion stops before it would overflow)
 constexpr int kRec = 64;    // record ring, >= 31 + 32 pending records
@@ -620,12 +619,13 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
 // flattened-quad scan, filter and candidate ring as K2.  A list longer than kHubMax keeps only
 // the filter; its candidates are verified by binary search in global memory.
 constexpr int kHubMax = 8192;
-constexpr int kHubRing = 256;  // >= 31 + 32 * kQuad pending candidates
+constexpr int kHubQ = 8;        // items per lane: one aligned 32-byte sector (one LDG.E.256)
+constexpr int kHubRing = 512;   // >= 31 + 32 * kHubQ pending candidates
 constexpr int kHubFilterLog = 16;
 constexpr int kHubFilterWords = (1 << kHubFilterLog) / 32;
 
 struct K2HubWarp {
-    int4 seg[32];  // per lane: {start of N+(v) & ~3 - 4 * first quad, end, start, 0}
+    int4 seg[32];  // per lane: {start of N+(v) & ~7 - 8 * first sector, end, start, 0}
     int owner[32];
     int ring[kHubRing];
 };
@@ -691,12 +691,12 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                 const int v = staged ? H.list[s - A] : col_or[s];
                 vs = rp_or[v];
                 vd = rp_or[v + 1] - vs;
-                wt = (vs + vd - (vs & ~3) + kQuad - 1) / kQuad;  // 16-byte aligned quads
+                wt = (vs + vd - (vs & ~7) + kHubQ - 1) / kHubQ;  // aligned 32-byte sectors
             }
             const int incl = warp_incl_scan(wt, lane);
             const int total = __shfl_sync(FULL, incl, 31);
             const int pre = incl - wt;
-            W.seg[lane] = make_int4((vs & ~3) - kQuad * pre, vs + vd, vs, 0);
+            W.seg[lane] = make_int4((vs & ~7) - kHubQ * pre, vs + vd, vs, 0);
             const unsigned nz = __ballot_sync(FULL, wt > 0);
             int cur = nz ? __ffs(nz) - 1 : 0;
             int head = 0, tail = 0;
@@ -710,22 +710,22 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                 const int own = W.owner[31 - __clz(mine | 1u)];
                 const int jj = mine ? own : cur;  // lanes past the end: jj's segment, masked
                 const int4 sg = W.seg[jj];
-                const int sv0 = sg.x + kQuad * (k0 + lane);  // 16-byte aligned
-                const int4 q4 = __ldg(reinterpret_cast<const int4*>(
-                    col_or + min(sv0, (sg.y - 1) & ~3)));
-                const int wq[kQuad] = {q4.x, q4.y, q4.z, q4.w};
+                const int sv0 = sg.x + kHubQ * (k0 + lane);  // 32-byte aligned
+                TWC_ASSERT(min(sv0, (sg.y - 1) & ~7) >= 0);
+                int wq[kHubQ];
+                ldg_sector(col_or + min(sv0, (sg.y - 1) & ~7), wq);
                 unsigned cm = 0;
 #pragma unroll
-                for (int e = 0; e < kQuad; ++e) {
+                for (int e = 0; e < kHubQ; ++e) {
                     const unsigned x = (unsigned)wq[e] * kFiltK;
                     const unsigned word = H.filt[hub_word(x)];
                     cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
                 }
-                cm &= ((1u << min(max(sg.y - sv0, 0), kQuad)) - 1u) &
-                      (0xfu << min(max(sg.z - sv0, 0), kQuad));
+                cm &= ((1u << min(max(sg.y - sv0, 0), kHubQ)) - 1u) &
+                      (0xffu << min(max(sg.z - sv0, 0), kHubQ));
                 const int cbase = (jj << 16) + (sv0 - sg.z);  // + e >= 0 for a valid entry
 #pragma unroll
-                for (int e = 0; e < kQuad; ++e) {
+                for (int e = 0; e < kHubQ; ++e) {
                     const bool c = (cm >> e) & 1u;
                     const unsigned b = __ballot_sync(FULL, c);
                     if (c) W.ring[(tail + __popc(b & lt_mask)) & (kHubRing - 1)] = cbase + e;
