@@ -19,6 +19,15 @@ namespace twc {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// One aligned 32-byte sector of an oriented list per lane: a single 256-bit load (LDG.E.256, sm_100)
+// instead of two 128-bit loads touching the same lines twice.
+__device__ __forceinline__ void ldg_sector(const int* p, int (&w)[8]) {
+    asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+          "=r"(w[7])
+        : "l"(p));
+}
+
 // Largest index i in [0, len) with a[i] <= x, given a sorted ascending and a[0] <= x.
 template <typename T, typename U>
 __device__ __forceinline__ int last_le(const T* a, int len, U x) {

@@ -197,9 +197,8 @@ __device__ __forceinline__ void k4_group_pass(K4GroupSmem<W>& S, int lane, int l
             const int jj = mine ? own : cur;
             const int4 sg = S.seg[jj];
             const int sv0 = sg.x + 8 * (k0 + lane);  // 32-byte aligned
-            const int4* src = reinterpret_cast<const int4*>(col_or + min(sv0, (sg.y - 1) & ~7));
-            const int4 qa = __ldg(src), qb = __ldg(src + 1);
-            const int y[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+            int y[8];
+            ldg_sector(col_or + min(sv0, (sg.y - 1) & ~7), y);  // one LDG.E.256
             unsigned cm = 0;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {

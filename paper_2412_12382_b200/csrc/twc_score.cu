@@ -390,14 +390,6 @@ struct K2WarpSmem {
 template <int FLOG>
 __device__ __forceinline__ unsigned filter_word(unsigned x) { return x >> (32 - FLOG + 5); }
 
-// One aligned 32-byte sector of col_or per lane: a single 256-bit load (LDG.E.256, sm_100)
-// instead of two 128-bit loads touching the same lines twice.
-__device__ __forceinline__ void ldg_sector(const int* p, int (&w)[8]) {
-    asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
-          "=r"(w[7])
-        : "l"(p));
-}
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
