@@ -392,8 +392,6 @@ struct FusedWs {
     int2 *kept, *pairs;
     unsigned short* kband;
     unsigned long long* stats;
-    int4* rev;  // K3's reversed edges (second pass)
-    int* nrev;
 };
 
 static FusedWs carve_fused(Carver& cv, int64_t n, int64_t m) {
@@ -411,8 +409,6 @@ static FusedWs carve_fused(Carver& cv, int64_t n, int64_t m) {
     w.pairs = cv.take<int2>(m);
     w.kband = cv.take<unsigned short>(m);
     w.stats = cv.take<unsigned long long>(2 * kMaxK);
-    w.rev = cv.take<int4>(m);
-    w.nrev = cv.take<int>(1);
     return w;
 }
 
@@ -446,8 +442,7 @@ cudaError_t score_sweep_impl(int64_t n, int64_t m, const RP* rowptr, const int* 
     sweep_upload(P, w.thr, w.order, s);
     cudaMemsetAsync(w.cnt, 0, sizeof(int) * (k + 1), s);
     cudaMemsetAsync(w.nkept, 0, sizeof(int), s);
-    cudaMemsetAsync(w.nrev, 0, sizeof(int), s);
-    BinSpec bin{w.thr, k, w.cnt, w.nkept, w.kept, w.kband, w.parent, w.rev, w.nrev};
+    BinSpec bin{w.thr, k, w.cnt, w.nkept, w.kept, w.kband, w.parent};  // K0 initialises parent
     cudaError_t e = score_impl<RP>(n, m, rowptr, colidx, w.score, w.score_bytes, t, wedge, tw, s,
                                    ev, &bin);
     if (e != cudaSuccess) return e;

@@ -87,8 +87,6 @@ struct BinSpec {
     int2* kept;             // device [m] (u, v) of kept edges, in no particular order
     unsigned short* kband;  // device [m] band of kept[i]
     int* parent = nullptr;  // device [n] or NULL: union-find parents, initialised by K0 (parent[u] = u)
-    int4* rev = nullptr;    // device [m] or NULL: K3's reversed edges for its second pass
-    int* nrev = nullptr;    // device counter of rev (zeroed by the caller)
 };
 size_t score_ws_bytes(int64_t n, int64_t m);
 

@@ -13,7 +13,6 @@
 // count arrays, which one int32 array plus atomics avoids on a GPU.  DESIGN.md Sec. 4.
 #include <algorithm>
 #include <climits>
-#include <cstdlib>
 #include <vector>
 
 #include "twc_common.cuh"
@@ -808,9 +807,7 @@ constexpr int kMaxTileRows = 2048;
 // canonical edges of the rank's slice [cb[rank], cb[rank+1]); an edge whose oriented slot lies
 // outside the rank's oriented slice [ob[rank], ob[rank+1]) (a reversed edge whose far endpoint
 // belongs to another rank) is not scored here but recorded as {c, u, v, slot} for the owner.
-// SPLIT: every reversed edge is recorded {c, u, v, d_u + d_v} (into dist.rec / dist.nrec) and left
-// to k3_reversed, which resolves several of them per thread at once; this kernel then streams.
-template <typename RP, bool BIN, bool K4 = false, bool DIST = false, bool SPLIT = false>
+template <typename RP, bool BIN, bool K4 = false, bool DIST = false>
 __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
     int64_t n, int64_t m, const RP* __restrict__ rowptr, const int* __restrict__ colidx,
     const int2* __restrict__ vinfo, const unsigned short* __restrict__ dslot,
@@ -882,21 +879,17 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
             const unsigned ow = obits[wi];
             int dv = __ldcs(dslot + p);
             if (dv == 0xffff) dv = deg[v];  // saturated: a vertex of degree >= 65535
-            int sl = 0;
+            int sl;
             if ((ow >> (p & 31)) & 1u) {
                 // aligned: oriented slot = #out-slots before p (word prefix + popc)
                 sl = opre[wi] + __popc(ow & ((1u << (p & 31)) - 1u));
-            } else if (SPLIT) {  // reversed: resolved by k3_reversed
-                remote = true;
-                rrec = make_int4(c, u, v, du + dv);
             } else {  // reversed edge: u's position in N+(v), one random 8-byte record first
                 const int2 vi = vinfo[v];
                 sl = sector_search(col_or, vi.x, vi.y, u, n);
             }
             TWC_ASSERT(sl >= 0 && (int64_t)sl < m);
-            TWC_ASSERT(SPLIT || ((ow >> (p & 31)) & 1u) || col_or[sl] == u);  // search found u
-            if (SPLIT && remote) {
-            } else if (DIST && (sl < o_lo || sl >= o_hi)) {  // counted by another rank: ask its owner
+            TWC_ASSERT(((ow >> (p & 31)) & 1u) || col_or[sl] == u);  // the reversed search found u
+            if (DIST && (sl < o_lo || sl >= o_hi)) {  // counted by another rank: ask its owner
                 remote = true;
                 rrec = make_int4(c, u, v, sl);
             } else {
@@ -914,7 +907,7 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
             }
             }  // local edge
             }
-            if (DIST || SPLIT) {  // warp-aggregated append of the remote / reversed edges
+            if (DIST) {  // warp-aggregated append of the remote edges
                 const unsigned rb = __ballot_sync(FULL, remote);
                 if (rb) {
                     int base = 0;
@@ -959,116 +952,6 @@ __global__ void __launch_bounds__(kK3Threads, 8) k3_score(
         for (int i = threadIdx.x; i < bin.k; i += blockDim.x)
             if (s_hist[i]) atomicAdd(&bin.cnt[i], s_hist[i]);
     }
-}
-
-// K3 second pass (SPLIT): the reversed edges recorded by k3_score<..., SPLIT>, R per thread with
-// their dependent random reads -- vinfo[v], the sector search of u in N+(v), t_or[slot] -- issued
-// for all R at once (R independent chains in flight per thread instead of one).  Outputs and the
-// binning of kept edges as in k3_score.
-template <int R>
-__global__ void __launch_bounds__(kK3Threads, R == 2 ? 6 : 4) k3_reversed(
-    int64_t n, const int4* __restrict__ rec, const int* __restrict__ nrec,
-    const int2* __restrict__ vinfo, const int* __restrict__ col_or, const int* __restrict__ t_or,
-    int* __restrict__ t, int* __restrict__ wedge, int* __restrict__ tw, BinSpec bin) {
-    extern __shared__ __align__(8) unsigned char rev_dyn[];  // thr[k] (i64), hist[k]
-    long long* s_thr = reinterpret_cast<long long*>(rev_dyn);
-    int* s_hist = reinterpret_cast<int*>(rev_dyn + 8 * (size_t)bin.k);
-    for (int i = threadIdx.x; i < bin.k; i += blockDim.x) {
-        s_thr[i] = bin.thr[i];
-        s_hist[i] = 0;
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int N = *nrec;
-    for (int base = blockIdx.x * blockDim.x * R; base < N; base += gridDim.x * blockDim.x * R) {
-        int c[R], u[R], v[R], s[R], lo[R], hi[R], sl[R];
-#pragma unroll
-        for (int j = 0; j < R; ++j) {  // records of the chunk, coalesced
-            const int i = base + j * blockDim.x + threadIdx.x;
-            const int4 r = i < N ? rec[i] : make_int4(-1, 0, 0, 0);
-            c[j] = r.x;
-            u[j] = r.y;
-            v[j] = r.z;
-            sl[j] = r.w;  // d_u + d_v until the slot is found
-        }
-        int ob[R], oe[R];
-#pragma unroll
-        for (int j = 0; j < R; ++j) {  // R independent vinfo loads
-            const int2 vi = c[j] >= 0 ? vinfo[v[j]] : make_int2(0, 1);
-            ob[j] = vi.x;
-            oe[j] = vi.y;
-        }
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            const int len = oe[j] - ob[j];
-            lo[j] = ob[j] & ~7;
-            hi[j] = (oe[j] - 1) & ~7;
-            s[j] = max(lo[j], min((ob[j] + (int)(((long long)len * u[j]) / n)) & ~7, hi[j]));
-        }
-        unsigned pend = 0;
-#pragma unroll
-        for (int j = 0; j < R; ++j) pend |= (c[j] >= 0 ? 1u : 0u) << j;
-        int dsum[R];
-#pragma unroll
-        for (int j = 0; j < R; ++j) dsum[j] = sl[j];
-        while (pend) {  // interpolated sector searches, all pending chains one step at a time
-#pragma unroll
-            for (int j = 0; j < R; ++j) {
-                if ((pend >> j) & 1u) {
-                    TWC_ASSERT(s[j] >= lo[j] && s[j] <= hi[j] && s[j] >= 0);
-                    int x[8];
-                    ldg_sector(col_or + s[j], x);
-                    const int first = max(ob[j] - s[j], 0), last = min(oe[j] - s[j], 8) - 1;
-                    int fv = 0, lv = 0, below = 0;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        fv = (e == first) ? x[e] : fv;
-                        lv = (e == last) ? x[e] : lv;
-                        below += (e >= first && e <= last && x[e] < u[j]);
-                    }
-                    if (s[j] > lo[j] && fv > u[j]) {
-                        s[j] -= 8;
-                    } else if (s[j] < hi[j] && lv < u[j]) {
-                        s[j] += 8;
-                    } else {
-                        sl[j] = s[j] + first + below;
-                        pend &= ~(1u << j);
-                    }
-                }
-            }
-        }
-        int tt[R];
-#pragma unroll
-        for (int j = 0; j < R; ++j) tt[j] = c[j] >= 0 ? t_or[sl[j]] : 0;  // R independent gathers
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            int b = -1 - lane;  // unique dummy for lanes without a kept edge
-            if (c[j] >= 0) {
-                TWC_ASSERT(col_or[sl[j]] == u[j]);
-                const int score = 3 * tt[j] - dsum[j] + 2;          // Eq. 2 with P:337
-                __stcs(t + c[j], tt[j]);
-                __stcs(wedge + c[j], dsum[j] - 2 * tt[j] - 2);
-                __stcs(tw + c[j], score);
-                if ((long long)score >= s_thr[bin.k - 1]) b = band_of(score, s_thr, bin.k);
-            }
-            const unsigned kb = __ballot_sync(FULL, b >= 0);
-            if (kb) {  // one reservation per warp, one smem atomic per distinct band
-                int wpos = 0;
-                if (lane == __ffs(kb) - 1) wpos = atomicAdd(bin.nkept, __popc(kb));
-                wpos = __shfl_sync(FULL, wpos, __ffs(kb) - 1);
-                const unsigned grp = __match_any_sync(FULL, b);
-                if (b >= 0) {
-                    const int pos = wpos + __popc(kb & ((1u << lane) - 1u));
-                    bin.kept[pos] = make_int2(u[j], v[j]);
-                    bin.kband[pos] = (unsigned short)b;
-                    if (lane == __ffs(grp) - 1) atomicAdd(&s_hist[b], __popc(grp));
-                }
-            }
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < bin.k; i += blockDim.x)
-        if (s_hist[i]) atomicAdd(&bin.cnt[i], s_hist[i]);
 }
 
 // ------------------------------------------------------------------------ host side
@@ -1155,16 +1038,6 @@ constexpr int kK2MinBlocks = 5;
 #define K2_KERNEL k2_intersect<kOct, kK2FilterLog, kK2MinBlocks>
 using K2Smem = K2WarpSmem<kK2FilterLog>;
 
-
-// K3 split into a streaming pass and a pass over the reversed edges with R chains per thread:
-// TWC_K3SPLIT = 0 (one pass), 2 or 4 (A/B), read once per process.
-static int k3_split() {
-    static const int v = [] {
-        const char* e = getenv("TWC_K3SPLIT");
-        return e ? atoi(e) : 0;
-    }();
-    return v;
-}
 
 // Stage A: degrees, orientation + oriented CSR (K0, K1) and the intersection (K2h, K2) of all
 // pivots, or of a shard's pivot range.  Events [0] start, [1] orientation done, [2] K2 done.
@@ -1261,23 +1134,7 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
             k3_score<RP, false, true><<<grid, kK3Threads, 0, s>>>(
                 n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre,
                 w.obits, w.t_or, t, wedge, tw, BinSpec{}, k4_or, k4);
-        else if (bin && bin->rev && k3_split() > 0) {
-            // streaming pass (aligned edges) + the reversed edges R per thread
-            DistK3 d;
-            d.rec = bin->rev;
-            d.nrec = bin->nrev;
-            k3_score<RP, true, false, false, true><<<grid, kK3Threads, k3_bin_smem(bin->k), s>>>(
-                n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre,
-                w.obits, w.t_or, t, wedge, tw, *bin, nullptr, nullptr, d);
-            const size_t rs = (size_t)bin->k * 12;
-            if (k3_split() == 2)
-                k3_reversed<2><<<sms * 8, kK3Threads, rs, s>>>(n, bin->rev, bin->nrev, w.vinfo,
-                                                              w.col_or, w.t_or, t, wedge, tw, *bin);
-            else
-                k3_reversed<4><<<sms * 8, kK3Threads, rs, s>>>(n, bin->rev, bin->nrev, w.vinfo,
-                                                              w.col_or, w.t_or, t, wedge, tw, *bin);
-            count_launches(1);
-        } else if (bin)
+        else if (bin)
             k3_score<RP, true><<<grid, kK3Threads, k3_bin_smem(bin->k), s>>>(
                 n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
                 wedge, tw, *bin);
