@@ -2,12 +2,16 @@
 # A/B of library variants selected by an environment variable (same build): per value, the
 # parity tests under that value, the kernel-only bench line, and a short ncu pass on the
 # kernel(s) of interest.
-# usage: bash scripts/gpu_ab_vars.sh TAG VAR "v0 v1 ..." [KERNEL_REGEX] [PYTEST_ARGS]
-TAG=$1; VAR=$2; VALS=$3; KRE=${4:-k2_intersect}; PT=${5:-tests/test_gpu_parity.py}
+# usage: bash scripts/gpu_ab_vars.sh TAG VAR "v0 v1 ..." [KERNEL_REGEX] [PYTEST_FILE|none] [-k EXPR]
+TAG=$1; VAR=$2; VALS=$3; KRE=${4:-k2_intersect}; PT=${5:-tests/test_gpu_parity.py}; KX=${6:-}
 mkdir -p gpurun_out
 for v in $VALS; do
   if [ "$PT" != none ]; then
-    env $VAR=$v timeout 900 python -m pytest $PT -x -q > gpurun_out/pytest_${TAG}_$v.log 2>&1
+    if [ -n "$KX" ]; then
+      env $VAR=$v timeout 900 python -m pytest $PT -x -q -k "$KX" > gpurun_out/pytest_${TAG}_$v.log 2>&1
+    else
+      env $VAR=$v timeout 900 python -m pytest $PT -x -q > gpurun_out/pytest_${TAG}_$v.log 2>&1
+    fi
     rc=$?; echo "$VAR=$v pytest_exit=$rc"; tail -2 gpurun_out/pytest_${TAG}_$v.log
     [ $rc -eq 0 ] || continue
   fi
