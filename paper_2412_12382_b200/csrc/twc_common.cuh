@@ -51,16 +51,16 @@ __device__ __forceinline__ int lower_bound(const T* a, int len, T x) {
 }
 
 // Branch-light lower bound for short sorted lists (membership probes in smem).
+// (integer offsets, not a moving pointer: no 64-bit address arithmetic in the loop)
 template <typename T>
 __device__ __forceinline__ int lower_bound_bl(const T* a, int len, T x) {
-    const T* base = a;
-    int n = len;
+    int lo = 0, n = len;
     while (n > 1) {
-        int half = n >> 1;
-        base = (base[half - 1] < x) ? base + half : base;
+        const int half = n >> 1;
+        lo = (a[lo + half - 1] < x) ? lo + half : lo;
         n -= half;
     }
-    return (int)(base - a) + ((n == 1 && *base < x) ? 1 : 0);
+    return lo + ((n == 1 && a[lo] < x) ? 1 : 0);
 }
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {

@@ -433,15 +433,15 @@ __device__ __forceinline__ int k2_expand(SM& S, int lane, int rhead, int cnt, in
     const int incl = warp_incl_scan(nc, lane);
     const bool fits = lane < cnt && incl <= SM::kRingN - (tail - head);
     const unsigned fb = __ballot_sync(FULL, fits);
-    if (fits) {
+    if (fits) {  // a loop over the set bits: most records hold one candidate (max ~2-3 per warp)
         int pos = tail + incl - nc;
         const int tag = r.y >> 8;
-#pragma unroll
-        for (int e = 0; e < Q; ++e) {
-            if ((cm >> e) & 1u) {
-                S.ring[pos & (SM::kRingN - 1)] = make_int2(r.x + e, tag);
-                ++pos;
-            }
+        unsigned bits = cm;
+        while (bits) {
+            const int e = __ffs(bits) - 1;
+            bits &= bits - 1u;
+            S.ring[pos & (SM::kRingN - 1)] = make_int2(r.x + e, tag);
+            ++pos;
         }
     }
     const int used = __popc(fb);
