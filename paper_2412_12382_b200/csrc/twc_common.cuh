@@ -28,6 +28,13 @@ __device__ __forceinline__ void ldg_sector(const int* p, int (&w)[8]) {
         : "l"(p));
 }
 
+// Position of the most significant set bit of x != 0 (bfind: one FLO instead of clz + 31 - clz).
+__device__ __forceinline__ int msb_pos(unsigned x) {
+    int r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+
 // Largest index i in [0, len) with a[i] <= x, given a sorted ascending and a[0] <= x.
 template <typename T, typename U>
 __device__ __forceinline__ int last_le(const T* a, int len, U x) {

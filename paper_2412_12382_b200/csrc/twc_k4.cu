@@ -193,7 +193,7 @@ __device__ __forceinline__ void k4_group_pass(K4GroupSmem<W>& S, int lane, int l
             const unsigned bits = __reduce_or_sync(FULL, starts ? (1u << (pre - k0)) : 0u);
             __syncwarp();
             const unsigned mine = bits & ((2u << lane) - 1u);
-            const int own = S.owner[31 - __clz(mine | 1u)];
+            const int own = S.owner[msb_pos(mine | 1u)];
             const int jj = mine ? own : cur;
             const int4 sg = S.seg[jj];
             const int sv0 = sg.x + 8 * (k0 + lane);  // 32-byte aligned

@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
                         __reduce_or_sync(FULL, starts ? (1u << (pre - k0)) : 0u);
                     __syncwarp();
                     const unsigned mine = bits & ((2u << lane) - 1u);
-                    const int own = S.owner[31 - __clz(mine | 1u)];
+                    const int own = S.owner[msb_pos(mine | 1u)];
                     // lanes past the last quad belong to the last segment and get nval <= 0
                     const int jj = mine ? own : cur;
                     TWC_ASSERT(jj >= 0 && jj < 32);
@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                 const unsigned bits = __reduce_or_sync(FULL, starts ? (1u << (pre - k0)) : 0u);
                 __syncwarp();
                 const unsigned mine = bits & ((2u << lane) - 1u);
-                const int own = W.owner[31 - __clz(mine | 1u)];
+                const int own = W.owner[msb_pos(mine | 1u)];
                 const int jj = mine ? own : cur;  // lanes past the end: jj's segment, masked
                 const int4 sg = W.seg[jj];
                 const int sv0 = sg.x + kHubQ * (k0 + lane);  // 32-byte aligned
