@@ -35,6 +35,13 @@ __device__ __forceinline__ int msb_pos(unsigned x) {
     return r;
 }
 
+// Mask of the bits [lo, hi) (empty when hi <= lo; lo, hi in [0, 32]): one BMSK.
+__device__ __forceinline__ unsigned bit_range(int lo, int hi) {
+    unsigned r;
+    asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(r) : "r"(lo), "r"(max(hi - lo, 0)));
+    return r;
+}
+
 // Largest index i in [0, len) with a[i] <= x, given a sorted ascending and a[0] <= x.
 template <typename T, typename U>
 __device__ __forceinline__ int last_le(const T* a, int len, U x) {

@@ -584,8 +584,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
                         cm |= __funnelshift_r(word, word, x - (unsigned)e) & (1u << e);
                     }
                     // valid entries: sg.w <= sv0 + e < sg.y
-                    cm &= ((1u << min(max(sg.y - sv0, 0), Q)) - 1u) &
-                          (((1u << Q) - 1u) << min(max(sg.w - sv0, 0), Q));
+                    cm &= bit_range(max(sg.w - sv0, 0), min(sg.y - sv0, Q));
                     const unsigned hb = __ballot_sync(FULL, cm != 0u);
                     if (cm) S.rec[(rtail + __popc(hb & lt_mask)) & (kRec - 1)] =
                                 make_int2(sv0, (int)cm | (sg.z << 8));
