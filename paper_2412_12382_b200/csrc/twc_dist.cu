@@ -44,7 +44,7 @@ struct DistWs {
     void* score;          // the score workspace (oriented CSR, counts) -- kept between phases
     size_t score_bytes;
     int* bounds;          // [3 (world + 1)]: rows, oriented slice bounds, canonical slice bounds
-    int* ctr;             // [0] remote records, [1] kept edges, [2] forest pairs
+    int* ctr;             // [0] remote records, [1] kept edges
     int4* rec;            // remote reversed edges {c, u, v, slot}, as found
     int4* rec_g;          // the same grouped by owner (the order of the requests)
     int* tcnt;            // per-tile counts of the compaction, then their exclusive scan
@@ -56,7 +56,7 @@ struct DistWs {
     int2 *kept, *pairs;
     unsigned short* kband;
     int* parent;
-    int* fcum;            // forest pairs after each band (cumulative)
+    int* fcnt;            // forest pairs recorded in each band
     int2* gpairs;         // F: the P forests, band-segmented
     int* goff;            // F: band offsets into gpairs
     unsigned long long* stats;
@@ -85,7 +85,7 @@ static DistWs carve_dist(Carver& cv, int64_t n, int64_t m, int world) {
     w.pairs = cv.take<int2>(m);
     w.kband = cv.take<unsigned short>(m);
     w.parent = cv.take<int>(n);
-    w.fcum = cv.take<int>(kMaxK);
+    w.fcnt = cv.take<int>(kMaxK);
     w.gpairs = cv.take<int2>((size_t)world * (size_t)std::max<int64_t>(n - 1, 1));
     w.goff = cv.take<int>(kMaxK + 1);
     w.stats = cv.take<unsigned long long>(2 * kMaxK);
@@ -317,12 +317,22 @@ __global__ void __launch_bounds__(kDistThreads) k_finish_remote(
         if (s_hist[i]) atomicAdd(&bin.cnt[i], s_hist[i]);
 }
 
-// hooks of band b; every successful hook (a -> b) is recorded: the band's forest edges
+// hooks of band b; every successful hook (a -> b) is recorded: the band's forest edges, placed
+// after those of the earlier bands (their counts fcnt[0..b) are final: stream order)
 __global__ void __launch_bounds__(256) k_hook_record(const int2* __restrict__ pairs,
                                                      const int* __restrict__ off, int b,
                                                      int* __restrict__ parent,
                                                      int* __restrict__ forest,
-                                                     int* __restrict__ fpos, int64_t cap) {
+                                                     int* __restrict__ fcnt, int64_t cap) {
+    __shared__ int s_base[32];
+    int part = 0;
+    for (int j = threadIdx.x; j < b; j += blockDim.x) part += fcnt[j];
+    part = __reduce_add_sync(FULL, part);
+    if ((threadIdx.x & 31) == 0) s_base[threadIdx.x >> 5] = part;
+    __syncthreads();
+    int band_base = 0;
+    for (int wv = 0; wv < (int)(blockDim.x >> 5); ++wv) band_base += s_base[wv];
+    int* fpos = fcnt + b;
     const int beg = off[b], end = off[b + 1];
     const unsigned size = (unsigned)(end - beg);
     unsigned p2 = 1;  // scrambled visiting order as k_hook_list (twc_cluster.cu)
@@ -342,7 +352,7 @@ __global__ void __launch_bounds__(256) k_hook_record(const int2* __restrict__ pa
             if (lane == __ffs(hb) - 1) wpos = atomicAdd(fpos, __popc(hb));
             wpos = __shfl_sync(FULL, wpos, __ffs(hb) - 1);
             if (hooked) {
-                const int pos = wpos + __popc(hb & ((1u << lane) - 1u));
+                const int pos = band_base + wpos + __popc(hb & ((1u << lane) - 1u));
                 TWC_ASSERT(ra > rb && rb >= 0 && pos < cap);
                 forest[2 * pos] = ra;
                 forest[2 * pos + 1] = rb;
@@ -351,21 +361,20 @@ __global__ void __launch_bounds__(256) k_hook_record(const int2* __restrict__ pa
     }
 }
 
-__global__ void k_mark(const int* __restrict__ fpos, int* __restrict__ fcum, int b) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) fcum[b] = *fpos;
-}
-
 // outputs of E as int64 (the caller's collective buffers)
-__global__ void k_forest_sizes(int k, const int* __restrict__ fcum, const int* __restrict__ cnt,
-                               const int* __restrict__ fpos,
+__global__ void k_forest_sizes(int k, const int* __restrict__ fcnt, const int* __restrict__ cnt,
                                unsigned long long* __restrict__ forest_cum,
                                unsigned long long* __restrict__ kept_sizes,
                                unsigned long long* __restrict__ nforest) {
-    for (int i = threadIdx.x; i < k; i += blockDim.x) {
-        forest_cum[i] = (unsigned long long)fcum[i];
-        kept_sizes[i] = (unsigned long long)cnt[i];
+    for (int i = threadIdx.x; i < k; i += blockDim.x) kept_sizes[i] = (unsigned long long)cnt[i];
+    if (threadIdx.x == 0) {  // k <= 1024: one serial prefix
+        unsigned long long run = 0;
+        for (int i = 0; i < k; ++i) {
+            run += (unsigned long long)fcnt[i];
+            forest_cum[i] = run;
+        }
+        *nforest = run;
     }
-    if (threadIdx.x == 0) *nforest = (unsigned long long)*fpos;
 }
 
 // ---- F: the global sweep over the P forests ------------------------------------------------------
@@ -506,17 +515,16 @@ cudaError_t dist_forest_impl(int64_t n, int64_t m, int world, const long long* t
     band_offsets(w.cnt, k, w.order, w.off, w.cursor, w.stats, s);
     band_place(w.kept, w.kband, w.ctr + 1, m, k, w.cursor, w.pairs, s);
     init_parent(n, w.parent, s);
+    cudaMemsetAsync(w.fcnt, 0, sizeof(int) * (size_t)k, s);
     const int hook_grid = num_sms() * 8;
     for (int i = 0; i < k; ++i) {
         if (m > 0 && P.fresh[i]) {
-            k_hook_record<<<hook_grid, 256, 0, s>>>(w.pairs, w.off, i, w.parent, forest,
-                                                    w.ctr + 2, std::max<int64_t>(n - 1, 1));
+            k_hook_record<<<hook_grid, 256, 0, s>>>(w.pairs, w.off, i, w.parent, forest, w.fcnt,
+                                                    std::max<int64_t>(n - 1, 1));
             count_launches(1);
         }
-        k_mark<<<1, 32, 0, s>>>(w.ctr + 2, w.fcum, i);
-        count_launches(1);
     }
-    k_forest_sizes<<<1, 256, 0, s>>>(k, w.fcum, w.cnt, w.ctr + 2,
+    k_forest_sizes<<<1, 256, 0, s>>>(k, w.fcnt, w.cnt,
                                      reinterpret_cast<unsigned long long*>(forest_cum),
                                      reinterpret_cast<unsigned long long*>(kept_sizes),
                                      reinterpret_cast<unsigned long long*>(nforest));
