@@ -374,7 +374,7 @@ constexpr unsigned kFiltK = 2654435761u;
 
 // 4,368 bytes per warp at FLOG = 13: 5 CTAs of 8 warps fit the 196 KB smem carveout and leave
 // 60 KB of L1 (DESIGN.md Sec. 4.1 for the carveout / occupancy measurements).
-template <int FLOG, int RING = kRing>
+template <int FLOG, int RING = kRing, int SPL = 1>
 struct K2WarpSmem {
     static constexpr int kFilterWords = (1 << FLOG) / 32;
     static constexpr int kRingN = RING;
@@ -382,7 +382,7 @@ struct K2WarpSmem {
     unsigned filt[kFilterWords];
     int prp[33];                    // group pivot offsets rp_or[u0 .. u0+np]
     int owner[32];                  // quad-segment owner lookup
-    int4 seg[32];                   // per lane: {start of N+(v) - 4 * first quad, end, tag, 0}
+    int4 seg[32 * SPL];             // per slot of the round: {start of N+(v) - 8 * first sector, end, tag, start}
     int2 ring[RING];                // candidates: {slot of v -> w, tag}
     int2 rec[kRec];                 // candidate quads: {slot of the quad, mask | tag << 4}
 };
@@ -468,7 +468,11 @@ __device__ __forceinline__ void k2_drain(SM& S, int lane, int keep, int A, int& 
 }
 
 // range: NULL (all pivots) or device {u_lo, u_hi} of a shard (the queue starts at u_lo)
-template <int Q, int FLOG, int MINB, int RING = kRing>
+// SPL: slots per lane and round (a round takes 32 * SPL slots of the group and flattens their
+// sectors together).  SPL = 2 with a 64-entry candidate ring (same shared memory) was measured:
+// 1.82 ms against 1.765 ms for SPL = 1 -- the second owner test per window and the smaller ring
+// cost more instructions than the fuller last windows save (profiles/r2k_k2_experiments.md).
+template <int Q, int FLOG, int MINB, int RING = kRing, int SPL = 1>
 __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, int chunk,
                                                               const int* __restrict__ rp_or,
                                                               const int* __restrict__ col_or,
@@ -477,7 +481,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
                                                               const int* __restrict__ range,
                                                               const int2* __restrict__ vinfo) {
     extern __shared__ __align__(16) unsigned char k2_smem_raw[];
-    using SM = K2WarpSmem<FLOG, RING>;
+    using SM = K2WarpSmem<FLOG, RING, SPL>;
     SM* smem = reinterpret_cast<SM*>(k2_smem_raw);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -504,10 +508,18 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
             const int B = __shfl_sync(FULL, e_l, np - 1);
             TWC_ASSERT(np >= 1 && np <= 32 && B - A >= 0 && B - A <= kGroupSlots);
             TWC_ASSERT(fit == (np == 32 ? FULL : (1u << np) - 1u));  // a prefix of the pivots
+            // prp[] holds the ends of the group's NON-EMPTY lists only (list j = [prp[j], prp[j+1])),
+            // and lane j keeps prp[j+1] in a register: the list of a slot is then found with one
+            // ballot and one warp OR per round instead of a binary search in shared memory
+            int b_l = __shfl_up_sync(FULL, e_l, 1);
+            if (lane == 0) b_l = A;
+            const unsigned nem = __ballot_sync(FULL, lane < np && e_l > b_l);
+            const int npc = __popc(nem);
             if (lane == 0) S.prp[0] = A;
-            if (lane < np) S.prp[lane + 1] = e_l;
+            if ((nem >> lane) & 1u) S.prp[__popc(nem & lt_mask) + 1] = e_l;
             for (int i = lane; i < SM::kFilterWords; i += 32) S.filt[i] = 0u;
             __syncwarp();
+            const int E = (lane < npc) ? S.prp[lane + 1] : INT_MAX;
             for (int i = lane; i < B - A; i += 32) {
                 const int x = __ldcs(col_or + A + i);  // read once: staged, not kept in L1
                 S.list[i] = x;
@@ -517,45 +529,66 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
             __syncwarp();
             int head = 0, tail = 0;    // candidate ring
             int rhead = 0, rtail = 0;  // record ring
-            // ---- rounds of 32 slots
-            for (int r0 = A; r0 < B; r0 += 32) {
-                const int s = r0 + lane;
-                int wt = 0, vs = 0, vd = 0, pi = 0;
-                if (s < B) {
-                    const int v = S.list[s - A];
-                    pi = last_le(S.prp, np + 1, s);
-                    TWC_ASSERT(pi >= 0 && pi < np && S.prp[pi] <= s && s < S.prp[pi + 1]);
-                    if (S.prp[pi + 1] - S.prp[pi] >= 2) {
-                        const int2 vi = vinfo[v];  // {rp_or[v], rp_or[v+1]}: one 8-byte load
-                        vs = vi.x;
-                        vd = vi.y - vs;
-                        TWC_ASSERT(vs >= 0 && vd >= 0 && vd < 65536);
-                        // items in aligned groups of Q: [vs & ~(Q-1), vs + vd)
-                        wt = (vs + vd - (vs & ~(Q - 1)) + Q - 1) / Q;
+            // ---- rounds of 32 * SPL slots
+            for (int r0 = A; r0 < B; r0 += 32 * SPL) {
+                int wt[SPL], pre[SPL];
+                int total = 0, cur = -1;
+#pragma unroll
+                for (int k = 0; k < SPL; ++k) {
+                    const int sb = r0 + 32 * k;
+                    const int s = sb + lane;
+                    int w_ = 0, vs = 0, vd = 0, pi = 0;
+                    if (SPL == 1 || sb < B) {
+                        // list of slot s: #lists ending at or before s
+                        const int pbase = __popc(__ballot_sync(FULL, E <= sb));
+                        const unsigned bm = __reduce_or_sync(
+                            FULL, (E > sb && E < sb + 32) ? (1u << (E - sb)) : 0u);
+                        pi = pbase + __popc(bm & ((2u << lane) - 1u));
+                        if (s < B) {
+                            TWC_ASSERT(pi >= 0 && pi < npc && S.prp[pi] <= s && s < S.prp[pi + 1]);
+                            const int v = S.list[s - A];
+                            if (S.prp[pi + 1] - S.prp[pi] >= 2) {
+                                const int2 vi = vinfo[v];  // {rp_or[v], rp_or[v+1]}: one 8-byte load
+                                vs = vi.x;
+                                vd = vi.y - vs;
+                                TWC_ASSERT(vs >= 0 && vd >= 0 && vd < 65536);
+                                // items in aligned groups of Q: [vs & ~(Q-1), vs + vd)
+                                w_ = (vs + vd - (vs & ~(Q - 1)) + Q - 1) / Q;
+                            }
+                        }
                     }
+                    const int incl = warp_incl_scan(w_, lane);
+                    wt[k] = w_;
+                    pre[k] = total + incl - w_;
+                    S.seg[32 * k + lane] =
+                        make_int4((vs & ~(Q - 1)) - Q * pre[k], vs + vd, (s - A) | (pi << 8), vs);
+                    if (w_ > 0) {  // the sector loop below reads N+(v): L2 prefetch (3 % of K2)
+                        prefetch_l2(col_or + vs);
+                        if (((vs + vd - 1) >> 5) != (vs >> 5)) prefetch_l2(col_or + vs + vd - 1);
+                    }
+                    const unsigned nz = __ballot_sync(FULL, w_ > 0);
+                    if (cur < 0 && nz) cur = 32 * k + __ffs(nz) - 1;
+                    total += __shfl_sync(FULL, incl, 31);
                 }
-                const int incl = warp_incl_scan(wt, lane);
-                const int total = __shfl_sync(FULL, incl, 31);
-                const int pre = incl - wt;
-                S.seg[lane] = make_int4((vs & ~(Q - 1)) - Q * pre, vs + vd, (s - A) | (pi << 8), vs);
-                if (wt > 0) {  // the quad loop below reads N+(v)
-                    prefetch_l2(col_or + vs);
-                    if (((vs + vd - 1) >> 5) != (vs >> 5)) prefetch_l2(col_or + vs + vd - 1);
-                }
-                const unsigned nz = __ballot_sync(FULL, wt > 0);
-                int cur = nz ? __ffs(nz) - 1 : 0;
+                cur = max(cur, 0);
                 __syncwarp();
                 for (int k0 = 0; k0 < total; k0 += 32) {
-                    const bool starts = wt > 0 && pre >= k0 && pre < k0 + 32;
-                    if (starts) S.owner[pre - k0] = lane;
-                    const unsigned bits =
-                        __reduce_or_sync(FULL, starts ? (1u << (pre - k0)) : 0u);
+                    unsigned sb_ = 0;
+#pragma unroll
+                    for (int k = 0; k < SPL; ++k) {
+                        const bool starts = wt[k] > 0 && pre[k] >= k0 && pre[k] < k0 + 32;
+                        if (starts) {
+                            S.owner[pre[k] - k0] = 32 * k + lane;
+                            sb_ |= 1u << (pre[k] - k0);
+                        }
+                    }
+                    const unsigned bits = __reduce_or_sync(FULL, sb_);
                     __syncwarp();
                     const unsigned mine = bits & ((2u << lane) - 1u);
                     const int own = S.owner[msb_pos(mine | 1u)];
                     // lanes past the last quad belong to the last segment and get nval <= 0
                     const int jj = mine ? own : cur;
-                    TWC_ASSERT(jj >= 0 && jj < 32);
+                    TWC_ASSERT(jj >= 0 && jj < 32 * SPL);
                     const int4 sg = S.seg[jj];
                     const int sv0 = sg.x + Q * (k0 + lane);  // 4Q-byte aligned
                     TWC_ASSERT(min(sv0, (sg.y - 1) & ~(Q - 1)) >= 0 && (sv0 & (Q - 1)) == 0);
