@@ -51,14 +51,15 @@ _lib = None
 
 def load_library(path: str | None = None):
     """Load libtwc.so (raises OSError loudly when it was not built).  TWC_LIB=checked selects the
-    checked build libtwc_checked.so (device-side asserts, build.py)."""
+    checked build libtwc_checked.so (device-side asserts, build.py); TWC_LIB=<name> an A/B variant
+    libtwc_<name>.so built with `build.py --variant <name> -D...`."""
     global _lib
     if _lib is not None:
         return _lib
     if path is None:
         path = LIB_PATH
-        if os.environ.get("TWC_LIB") == "checked":
-            path = os.path.join(_HERE, "libtwc_checked.so")
+        if os.environ.get("TWC_LIB"):  # "checked", or an A/B variant built by build.py --variant
+            path = os.path.join(_HERE, f"libtwc_{os.environ['TWC_LIB']}.so")
     if not os.path.exists(path):
         raise OSError(f"{path} not found: build it with `python -m paper_2412_12382_b200.build` "
                       "(there is no CPU fallback)")

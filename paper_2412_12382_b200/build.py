@@ -39,12 +39,16 @@ def _stale(lib=LIB):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False, checked=False):
+def build(force=False, verbose=False, checked=False, variant=None, defines=()):
+    """variant: an A/B build libtwc_<variant>.so of the same sources with extra -D defines
+    (loaded with TWC_LIB=<variant>; measurement only, never the default library)."""
     lib = LIB_CHECKED if checked else LIB
+    if variant:
+        lib = os.path.join(HERE, f"libtwc_{variant}.so")
     if not force and not _stale(lib):
         return lib
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, *(["-DTWC_CHECKED"] if checked else []),
+    cmd = [NVCC, *FLAGS, *(["-DTWC_CHECKED"] if checked else []), *defines,
            *(["-Xptxas", "-v"] if verbose else []), "-o", tmp,
            *[os.path.join(CSRC, f) for f in SOURCES]]
     subprocess.check_call(cmd)
@@ -53,4 +57,6 @@ def build(force=False, verbose=False, checked=False):
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv, checked="--checked" in sys.argv))
+    _variant = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else None
+    print(build(force=True, verbose="--verbose" in sys.argv, checked="--checked" in sys.argv,
+                variant=_variant, defines=[a for a in sys.argv[1:] if a.startswith("-D")]))

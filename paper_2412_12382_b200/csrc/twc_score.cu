@@ -392,7 +392,7 @@ __device__ __forceinline__ unsigned filter_word(unsigned x) { return x >> (32 - 
 
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));  // (.L1 instead: no difference, 1.762 / 1.760 ms)
 }
 
 // Verify ring entries [head, head + cnt) (cnt <= 32; lane i takes entry head + i).
@@ -1006,7 +1006,7 @@ static int grid_for(int64_t items, int per_block, int max_blocks) {
 struct AuxStream {
     int dev = -1;
     cudaStream_t stream = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, begin = nullptr, zeroed = nullptr;
 };
 
 static AuxStream* aux_stream() {
@@ -1019,7 +1019,9 @@ static AuxStream* aux_stream() {
     a.dev = dev;
     if (cudaStreamCreateWithFlags(&a.stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.begin, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a.zeroed, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
     }
@@ -1081,6 +1083,17 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
     const int64_t m2 = 2 * m;
     const int64_t nst = (m2 + kSlotTile - 1) / kSlotTile;
     record(ev, 0, s);
+    // the oriented counts and the queue counters are zeroed on the library's side stream while K1
+    // runs (K1 is bound by its deg gathers, not by DRAM; the 4m-byte memset took 25 us between K1
+    // and K2); K2h follows on that stream, K2 waits for `zeroed`
+    AuxStream* ax = aux_stream();
+    cudaStream_t sh = ax ? ax->stream : s;
+    if (ax) {
+        cudaEventRecord(ax->begin, s);
+        cudaStreamWaitEvent(sh, ax->begin, 0);
+        cudaMemsetAsync(w.t_or, 0, sizeof(int) * (size_t)m, sh);
+        cudaEventRecord(ax->zeroed, sh);
+    }
     // a1 + a2: degrees, orientation, oriented CSR (bits + tile counts, tile scan, scatter, rows)
     k0_degrees<RP><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rowptr, w.deg, parent);
     count_launches(1);
@@ -1100,7 +1113,7 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
     tile_first_rows(w.eoff, (int)n, m, w.trow, s);
     // (zeroing t_or inside K1b's scatter was measured: k1_write 0.10 -> 0.29 ms; the memset is
     // a 140 MB streaming write, ~25 us)
-    cudaMemsetAsync(w.t_or, 0, sizeof(int) * (size_t)m, s);
+    if (!ax) cudaMemsetAsync(w.t_or, 0, sizeof(int) * (size_t)m, s);
     cudaMemsetAsync(w.work, 0, 2 * sizeof(int), s);
     cudaMemsetAsync(w.nhubs, 0, sizeof(int), s);
     const int* range = nullptr;  // a shard counts only the triangles of its pivot range
@@ -1118,11 +1131,10 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
     // forked from and joined back to s: they start first (the largest tasks) and the
     // persistent K2 grid fills the SM resources they leave, so neither kernel's tail idles
     // the GPU.  No work and an early exit when the graph has no hub.
-    AuxStream* ax = aux_stream();
-    cudaStream_t sh = ax ? ax->stream : s;
     if (ax) {
         cudaEventRecord(ax->fork, s);
         cudaStreamWaitEvent(sh, ax->fork, 0);
+        cudaStreamWaitEvent(s, ax->zeroed, 0);
     }
     k2_find_hubs<<<(unsigned)((n + 255) / 256), 256, 0, sh>>>(n, w.rp_or, w.hubs, w.nhubs, range);
     const size_t hsmem = sizeof(K2HubSmem);
