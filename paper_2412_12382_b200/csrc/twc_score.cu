@@ -344,8 +344,9 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
 //  * the group's slots are taken 32 at a time (one per lane, a "round"); slot u->v owns the
 //    items w in N+(v) if d+(u) >= 2, cut into groups of Q = kOct entries aligned to one 32-byte
 //    sector of col_or (covering [start & ~7, end)).  The groups of the 32 slots are flattened
-//    across the lanes (exclusive scan of the group counts; the segment owning a group is found
-//    with one __reduce_or_sync bit mask + one smem lookup), so each lane reads one aligned
+//    across the lanes (exclusive scan of the group counts; the segment records are stored
+//    compacted in slot order, so the segment owning a sector is the number of segments started
+//    at or before it: one __reduce_or_sync bit mask and a popc), so each lane reads one aligned
 //    sector (one 256-bit LDG.E.256) of one N+(v) and a warp reads a contiguous run.  The per-lane
 //    segment record {start & ~7 - 8 * first group, end, tag, start} gives a group's slots with
 //    one 16-byte smem load; loads are clamped into the list, so loads and hashes run
@@ -372,7 +373,7 @@ constexpr int kRing = 128;  // candidate ring, default (an expansion stops befor
 constexpr int kRec = 64;    // record ring, >= 31 + 32 pending records
 constexpr unsigned kFiltK = 2654435761u;
 
-// 4,368 bytes per warp at FLOG = 13: 5 CTAs of 8 warps fit the 196 KB smem carveout and leave
+// 4,240 bytes per warp at FLOG = 13: 5 CTAs of 8 warps fit the 196 KB smem carveout and leave
 // 60 KB of L1 (DESIGN.md Sec. 4.1 for the carveout / occupancy measurements).
 template <int FLOG, int RING = kRing, int SPL = 1>
 struct K2WarpSmem {
@@ -380,8 +381,7 @@ struct K2WarpSmem {
     static constexpr int kRingN = RING;
     int list[kGroupSlots];          // staged col_or[A, B)
     unsigned filt[kFilterWords];
-    int prp[33];                    // group pivot offsets rp_or[u0 .. u0+np]
-    int owner[32];                  // quad-segment owner lookup
+    int prp[33];                    // ends of the group's non-empty lists (list j = [prp[j], prp[j+1]))
     int4 seg[32 * SPL];             // per slot of the round: {start of N+(v) - 8 * first sector, end, tag, start}
     int2 ring[RING];                // candidates: {slot of v -> w, tag}
     int2 rec[kRec];                 // candidate quads: {slot of the quad, mask | tag << 4}
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
             // ---- rounds of 32 * SPL slots
             for (int r0 = A; r0 < B; r0 += 32 * SPL) {
                 int wt[SPL], pre[SPL];
-                int total = 0, cur = -1;
+                int total = 0, nseg = 0;
 #pragma unroll
                 for (int k = 0; k < SPL; ++k) {
                     const int sb = r0 + 32 * k;
@@ -560,35 +560,35 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
                     const int incl = warp_incl_scan(w_, lane);
                     wt[k] = w_;
                     pre[k] = total + incl - w_;
-                    S.seg[32 * k + lane] =
-                        make_int4((vs & ~(Q - 1)) - Q * pre[k], vs + vd, (s - A) | (pi << 8), vs);
-                    if (w_ > 0) {  // the sector loop below reads N+(v): L2 prefetch (3 % of K2)
+                    // the segments with sectors are stored compacted, in slot order = order of their
+                    // first sector: the j-th segment starting in a window is the (#segments
+                    // started before the window + j)-th record, so no owner table is needed
+                    const unsigned nz = __ballot_sync(FULL, w_ > 0);
+                    if (w_ > 0) {
+                        S.seg[nseg + __popc(nz & lt_mask)] =
+                            make_int4((vs & ~(Q - 1)) - Q * pre[k], vs + vd, (s - A) | (pi << 8), vs);
+                        // the sector loop below reads N+(v): L2 prefetch (3 % of K2)
                         prefetch_l2(col_or + vs);
                         if (((vs + vd - 1) >> 5) != (vs >> 5)) prefetch_l2(col_or + vs + vd - 1);
                     }
-                    const unsigned nz = __ballot_sync(FULL, w_ > 0);
-                    if (cur < 0 && nz) cur = 32 * k + __ffs(nz) - 1;
+                    nseg += __popc(nz);
                     total += __shfl_sync(FULL, incl, 31);
                 }
-                cur = max(cur, 0);
+                int cb = 0;  // segments started before the current window
                 __syncwarp();
                 for (int k0 = 0; k0 < total; k0 += 32) {
                     unsigned sb_ = 0;
 #pragma unroll
                     for (int k = 0; k < SPL; ++k) {
                         const bool starts = wt[k] > 0 && pre[k] >= k0 && pre[k] < k0 + 32;
-                        if (starts) {
-                            S.owner[pre[k] - k0] = 32 * k + lane;
-                            sb_ |= 1u << (pre[k] - k0);
-                        }
+                        if (starts) sb_ |= 1u << (pre[k] - k0);
                     }
                     const unsigned bits = __reduce_or_sync(FULL, sb_);
-                    __syncwarp();
-                    const unsigned mine = bits & ((2u << lane) - 1u);
-                    const int own = S.owner[msb_pos(mine | 1u)];
-                    // lanes past the last quad belong to the last segment and get nval <= 0
-                    const int jj = mine ? own : cur;
-                    TWC_ASSERT(jj >= 0 && jj < 32 * SPL);
+                    // segment of sector k0 + lane: the last one started at or before it (lanes past
+                    // the last sector get the last segment and an empty validity mask)
+                    const int jj = cb + __popc(bits & ((2u << lane) - 1u)) - 1;
+                    cb += __popc(bits);
+                    TWC_ASSERT(jj >= 0 && jj < nseg);
                     const int4 sg = S.seg[jj];
                     const int sv0 = sg.x + Q * (k0 + lane);  // 4Q-byte aligned
                     TWC_ASSERT(min(sv0, (sg.y - 1) & ~(Q - 1)) >= 0 && (sv0 & (Q - 1)) == 0);
@@ -623,11 +623,10 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
                                 make_int2(sv0, (int)cm | (sg.z << 8));
                     rtail += __popc(hb);
                     TWC_ASSERT(rtail - rhead <= kRec);
-                    cur = __shfl_sync(FULL, jj, 31);
                     __syncwarp();
                     k2_drain<Q>(S, lane, 31, A, rhead, rtail, head, tail, col_or, t_or);
                 }
-                __syncwarp();  // seg / owner are rewritten by the next round
+                __syncwarp();  // seg is rewritten by the next round
             }
             k2_drain<Q>(S, lane, 0, A, rhead, rtail, head, tail, col_or, t_or);
             if (tail > head) k2_verify(S, lane, head, tail - head, A, col_or, t_or);
@@ -1069,8 +1068,11 @@ __global__ void k_dist_bounds(int64_t n, int64_t m, const int* __restrict__ rp_o
 // A/B-tested in round 2 and lost).
 constexpr int kK2FilterLog = 13;
 constexpr int kK2MinBlocks = 5;
-#define K2_KERNEL k2_intersect<kOct, kK2FilterLog, kK2MinBlocks>
-using K2Smem = K2WarpSmem<kK2FilterLog>;
+#ifndef TWC_K2_SPL
+#define TWC_K2_SPL 1
+#endif
+#define K2_KERNEL k2_intersect<kOct, kK2FilterLog, kK2MinBlocks, kRing, TWC_K2_SPL>
+using K2Smem = K2WarpSmem<kK2FilterLog, kRing, TWC_K2_SPL>;
 
 
 // Stage A: degrees, orientation + oriented CSR (K0, K1) and the intersection (K2h, K2) of all
