@@ -162,6 +162,10 @@ __global__ void __launch_bounds__(256) k_hook_list(const int2* __restrict__ pair
         if (j >= size) continue;
         const int2 e = pairs[beg + j];
         TWC_ASSERT(e.x >= 0 && e.y >= 0 && e.x != e.y);
+        // equal parents: already in one tree (the previous step's finalize left every vertex
+        // pointing at its root, so this settles most edges inside an existing component with
+        // two reads instead of two root walks)
+        if (parent[e.x] == parent[e.y]) continue;
         uf_unite(parent, e.x, e.y);
     }
 }

@@ -648,8 +648,7 @@ constexpr int kHubFilterLog = 16;
 constexpr int kHubFilterWords = (1 << kHubFilterLog) / 32;
 
 struct K2HubWarp {
-    int4 seg[32];  // per lane: {start of N+(v) & ~7 - 8 * first sector, end, start, 0}
-    int owner[32];
+    int4 seg[32];  // per segment: {start of N+(v) & ~7 - 8 * first sector, end, start, slot's lane}
     int ring[kHubRing];
 };
 struct K2HubSmem {
@@ -719,19 +718,21 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
             const int incl = warp_incl_scan(wt, lane);
             const int total = __shfl_sync(FULL, incl, 31);
             const int pre = incl - wt;
-            W.seg[lane] = make_int4((vs & ~7) - kHubQ * pre, vs + vd, vs, 0);
+            // segment records compacted in slot order, as in K2: the segment of a sector is the
+            // number of segments started at or before it; .w keeps the slot's lane
             const unsigned nz = __ballot_sync(FULL, wt > 0);
-            int cur = nz ? __ffs(nz) - 1 : 0;
+            if (wt > 0)
+                W.seg[__popc(nz & lt_mask)] = make_int4((vs & ~7) - kHubQ * pre, vs + vd, vs, lane);
+            int cb = 0;
             int head = 0, tail = 0;
             __syncwarp();
             for (int k0 = 0; k0 < total; k0 += 32) {
                 const bool starts = wt > 0 && pre >= k0 && pre < k0 + 32;
-                if (starts) W.owner[pre - k0] = lane;
                 const unsigned bits = __reduce_or_sync(FULL, starts ? (1u << (pre - k0)) : 0u);
-                __syncwarp();
-                const unsigned mine = bits & ((2u << lane) - 1u);
-                const int own = W.owner[msb_pos(mine | 1u)];
-                const int jj = mine ? own : cur;  // lanes past the end: jj's segment, masked
+                // lanes past the end get the last segment and an empty mask
+                const int jj = cb + __popc(bits & ((2u << lane) - 1u)) - 1;
+                cb += __popc(bits);
+                TWC_ASSERT(jj >= 0 && jj < __popc(nz));
                 const int4 sg = W.seg[jj];
                 const int sv0 = sg.x + kHubQ * (k0 + lane);  // 32-byte aligned
                 TWC_ASSERT(min(sv0, (sg.y - 1) & ~7) >= 0);
@@ -755,14 +756,14 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                     tail += __popc(b);
                 }
                 TWC_ASSERT(tail - head <= kHubRing);
-                cur = __shfl_sync(FULL, jj, 31);
                 __syncwarp();
                 while (tail - head > 0 && (tail - head >= 32 || k0 + 32 >= total)) {
                     const int cnt = min(32, tail - head);
                     if (lane < cnt) {
                         const int e = W.ring[(head + lane) & (kHubRing - 1)];
-                        const int j = e >> 16;
-                        const int sv = W.seg[j].z + (e & 0xffff);  // slot of v -> w
+                        const int4 cs = W.seg[e >> 16];
+                        const int j = cs.w;                        // lane of the slot u -> v
+                        const int sv = cs.z + (e & 0xffff);        // slot of v -> w
                         const int w = col_or[sv];
                         const int* L = staged ? H.list : col_or + A;
                         const int q = staged ? lower_bound_bl(L, len, w) : lower_bound(L, len, w);
