@@ -61,14 +61,17 @@ def to_bytes(val, unit):
 def bench_identity(tag):
     """config / graph identity of the bench line captured in the same gpurun (gpurun_out/
     bench_TAG.json), so bench.py only uses this capture's DRAM bytes for the same graph."""
-    p = os.path.join(ROOT, "gpurun_out", f"bench_{tag}.json")
-    try:
-        d = json.loads(open(p).read().strip().splitlines()[-1])
-        c = d["config"]
-        return {"graph_sha256": c.get("graph_sha256"), "n": c.get("n"), "m": c.get("m"),
-                "workload": c.get("workload"), "bench_line": f"profiles/{tag}_bench.json"}
-    except Exception:
-        return {}
+    # the full bench line, else the plain run that preceded the ncu passes (same graph)
+    for name in (f"bench_{tag}.json", f"plain_{tag}.log"):
+        p = os.path.join(ROOT, "gpurun_out", name)
+        try:
+            d = json.loads(open(p).read().strip().splitlines()[-1])
+            c = d["config"]
+            return {"graph_sha256": c.get("graph_sha256"), "n": c.get("n"), "m": c.get("m"),
+                    "workload": c.get("workload"), "bench_line": f"profiles/{tag}_bench.json"}
+        except Exception:
+            continue
+    return {}
 
 
 def full_summary(tag, rep):
