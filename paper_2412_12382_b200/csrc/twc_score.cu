@@ -520,6 +520,8 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
             for (int i = lane; i < SM::kFilterWords; i += 32) S.filt[i] = 0u;
             __syncwarp();
             const int E = (lane < npc) ? S.prp[lane + 1] : INT_MAX;
+            // lists with a single entry own no items (a triangle needs two out-neighbours)
+            const unsigned single = __ballot_sync(FULL, lane < npc && E - S.prp[lane] < 2);
             for (int i = lane; i < B - A; i += 32) {
                 const int x = __ldcs(col_or + A + i);  // read once: staged, not kept in L1
                 S.list[i] = x;
@@ -531,7 +533,8 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
             int rhead = 0, rtail = 0;  // record ring
             // ---- rounds of 32 * SPL slots
             for (int r0 = A; r0 < B; r0 += 32 * SPL) {
-                int wt[SPL], pre[SPL];
+                int swin[SPL];       // window of the slot's first sector (-1: no sectors)
+                unsigned sbit[SPL];  // its position in that window, as a bit
                 int total = 0, nseg = 0;
 #pragma unroll
                 for (int k = 0; k < SPL; ++k) {
@@ -547,7 +550,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
                         if (s < B) {
                             TWC_ASSERT(pi >= 0 && pi < npc && S.prp[pi] <= s && s < S.prp[pi + 1]);
                             const int v = S.list[s - A];
-                            if (S.prp[pi + 1] - S.prp[pi] >= 2) {
+                            if (!((single >> pi) & 1u)) {
                                 const int2 vi = vinfo[v];  // {rp_or[v], rp_or[v+1]}: one 8-byte load
                                 vs = vi.x;
                                 vd = vi.y - vs;
@@ -558,15 +561,16 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
                         }
                     }
                     const int incl = warp_incl_scan(w_, lane);
-                    wt[k] = w_;
-                    pre[k] = total + incl - w_;
+                    const int pre = total + incl - w_;
+                    swin[k] = w_ > 0 ? pre >> 5 : -1;
+                    sbit[k] = 1u << (pre & 31);
                     // the segments with sectors are stored compacted, in slot order = order of their
                     // first sector: the j-th segment starting in a window is the (#segments
                     // started before the window + j)-th record, so no owner table is needed
                     const unsigned nz = __ballot_sync(FULL, w_ > 0);
                     if (w_ > 0) {
                         S.seg[nseg + __popc(nz & lt_mask)] =
-                            make_int4((vs & ~(Q - 1)) - Q * pre[k], vs + vd, (s - A) | (pi << 8), vs);
+                            make_int4((vs & ~(Q - 1)) - Q * pre, vs + vd, (s - A) | (pi << 8), vs);
                         // the sector loop below reads N+(v): L2 prefetch (3 % of K2)
                         prefetch_l2(col_or + vs);
                         if (((vs + vd - 1) >> 5) != (vs >> 5)) prefetch_l2(col_or + vs + vd - 1);
@@ -579,10 +583,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
                 for (int k0 = 0; k0 < total; k0 += 32) {
                     unsigned sb_ = 0;
 #pragma unroll
-                    for (int k = 0; k < SPL; ++k) {
-                        const bool starts = wt[k] > 0 && pre[k] >= k0 && pre[k] < k0 + 32;
-                        if (starts) sb_ |= 1u << (pre[k] - k0);
-                    }
+                    for (int k = 0; k < SPL; ++k) sb_ |= (swin[k] == (k0 >> 5)) ? sbit[k] : 0u;
                     const unsigned bits = __reduce_or_sync(FULL, sb_);
                     // segment of sector k0 + lane: the last one started at or before it (lanes past
                     // the last sector get the last segment and an empty validity mask)
