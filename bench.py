@@ -477,6 +477,12 @@ def main_b200(args):
         roofline["dram"] = {"achieved": dram_gbs, "unit": "GB/s", "frac": dram_gbs / peak,
                             "frac_of_8000": dram_gbs / 8000.0,
                             "traffic_over_algorithmic": traffic / k2_bytes}
+    if k2prof and k2prof.get("l2_sectors_per_launch"):
+        # SURVEY 8(d) figure 3: L2 traffic (32-byte sectors of the same capture) over the live time
+        roofline["l2"] = {"achieved": 32.0 * k2prof["l2_sectors_per_launch"] / k2_avg_s / 1e9,
+                          "unit": "GB/s", "hit_pct": k2prof.get("l2_hit_pct"),
+                          "lsu_pipe_pct": k2prof.get("lsu_pipe_pct"),
+                          "warp_execution_efficiency": (k2prof.get("threads_per_inst") or 0) / 32.0}
     if k2prof and k2prof.get("warp_inst_per_launch"):
         # K2 is co-limited by instruction issue and the L1/shared pipe: its
         # warp instructions per launch (same capture) over the live K2 time, against 4

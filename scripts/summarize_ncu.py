@@ -110,6 +110,16 @@ def full_summary(tag, rep):
                   "issue_active_pct": float(r[col["smsp__issue_active.avg.pct_of_peak_sustained_active"]]),
                   "duration": r[col["gpu__time_duration.sum"]] + " " + units[col["gpu__time_duration.sum"]],
                   "source": f"profiles/{tag}_ncu_full.md", **bench_identity(tag)}
+            for key, name2 in (("lts__t_sectors.sum", "l2_sectors_per_launch"),
+                               ("lts__t_sector_hit_rate.pct", "l2_hit_pct"),
+                               ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+                                "lsu_pipe_pct"),
+                               ("smsp__thread_inst_executed_per_inst_executed.ratio",
+                                "threads_per_inst")):
+                try:  # third bandwidth figure (L2) and the evidence counters
+                    k2[name2] = float(r[col[key]].replace(",", ""))
+                except (KeyError, ValueError):
+                    pass
     with open(os.path.join(PROF, f"{tag}_ncu_full.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     if k2:
