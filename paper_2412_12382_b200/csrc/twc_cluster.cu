@@ -146,9 +146,20 @@ __global__ void __launch_bounds__(kSweepThreads) k_band_scatter(
 // Hook the edges of band b (one step of the sweep).
 __global__ void __launch_bounds__(256) k_hook_list(const int2* __restrict__ pairs,
                                                    const int* __restrict__ off, int b,
-                                                   int* __restrict__ parent) {
+                                                   int* __restrict__ parent, int64_t n) {
     const int beg = off[b], end = off[b + 1];
     const unsigned size = (unsigned)(end - beg);
+    // A large first band unites singletons: with every thread of the GPU hooking at once, half of
+    // the CAS attempts fail (the root found is no longer a root) and the walks get long, so the
+    // band is taken by max(n / 8, size / 64, 32 Ki) threads only -- fewer concurrent hooks per
+    // vertex, still enough threads for the band's bulk (measured on configs 2-4 and the R-MAT
+    // graphs; config 3's sweep 0.24 -> 0.13 ms).
+    unsigned nblk = gridDim.x;
+    if (b == 0 && (int64_t)size * 16 >= n) {
+        const int64_t thr = max(max(n / 8, (int64_t)size / 64), (int64_t)32768);
+        nblk = (unsigned)min((int64_t)gridDim.x, (thr + blockDim.x - 1) / blockDim.x);
+    }
+    if (blockIdx.x >= nblk) return;
     // visit the band in a scrambled order so that edges sharing a vertex (neighbours in the
     // band, which keeps canonical row order) are not handled by neighbouring threads at the
     // same time: j = (i * odd) mod 2^p is a bijection of [0, 2^p) (2^p >= size); the j >= size
@@ -156,8 +167,7 @@ __global__ void __launch_bounds__(256) k_hook_list(const int2* __restrict__ pair
     unsigned p2 = 1;
     while (p2 < size) p2 <<= 1;
     const unsigned mask = p2 - 1u;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < p2;
-         i += gridDim.x * blockDim.x) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < p2; i += nblk * blockDim.x) {
         const unsigned j = (i * 2654435761u) & mask;
         if (j >= size) continue;
         const int2 e = pairs[beg + j];
@@ -337,7 +347,7 @@ void sweep_loop(int64_t n, int64_t m, const SweepPlan& P, const int2* pairs, con
     for (int i = 0; i < P.k; ++i) {
         const int idx = P.order[i];
         if (m > 0 && P.fresh[i]) {
-            k_hook_list<<<hook_grid, 256, 0, s>>>(pairs, off, i, parent);
+            k_hook_list<<<hook_grid, 256, 0, s>>>(pairs, off, i, parent, n);
             count_launches(1);
         }
         k_finalize<<<fin_grid, 256, 0, s>>>(n, parent, labels + (size_t)idx * n, st + 2 * idx + 1);
