@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
 // of it in shared memory, and its 8 warps take the pivot's slots 32 at a time with the same
 // flattened-quad scan, filter and candidate ring as K2.  A list longer than kHubMax keeps only
 // the filter; its candidates are verified by binary search in global memory.
-constexpr int kHubMax = 8192;
+constexpr int kHubMax = 2048;
 constexpr int kHubQ = 8;        // items per lane: one aligned 32-byte sector (one LDG.E.256)
 constexpr int kHubRing = 512;   // >= 31 + 32 * kHubQ pending candidates
 constexpr int kHubFilterLog = 16;
@@ -654,7 +654,6 @@ struct K2HubWarp {
 };
 struct K2HubSmem {
     int list[kHubMax];
-    int cnt[kHubMax];
     unsigned filt[kHubFilterWords];
     K2HubWarp w[kK2Warps];
     int hub;
@@ -678,7 +677,12 @@ __global__ void k2_find_hubs(int64_t n, const int* __restrict__ rp_or, int* __re
     if (hub) hubs[base + __popc(b & ((1u << lane) - 1u))] = (int)u;
 }
 
-__global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
+// 6 CTAs per SM (40 registers, 36 KB of shared memory each): the hub kernel is latency-bound like
+// K2, and R-MAT dense 10^8 went 121.6 -> 98.5 ms when the per-entry shared counters (32 KB) were
+// replaced by global REDs (3 CTAs/SM instead of 2), -> 83.1 / 74.8 / 71.5 ms with 4,096 / 4,096 /
+// 2,048 staged entries at 4 / 5 / 6 CTAs/SM (profiles/r2k_k2_experiments.md Sec. 10).
+constexpr int kHubMinBlocks = 6;
+__global__ void __launch_bounds__(kK2Warps * 32, kHubMinBlocks) k2_hubs(
     const int* __restrict__ rp_or, const int* __restrict__ col_or, const int* __restrict__ hubs,
     const int* __restrict__ nhubs, int* __restrict__ work, int* __restrict__ t_or) {
     extern __shared__ __align__(16) unsigned char k2h_smem_raw[];
@@ -701,7 +705,6 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
             const int x = col_or[A + i];
             if (staged) {
                 H.list[i] = x;
-                H.cnt[i] = 0;
             }
             const unsigned hx = (unsigned)x * kFiltK;
             atomicOr(&H.filt[hub_word(hx)], 1u << (hx & 31));
@@ -770,13 +773,8 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
                         const int q = staged ? lower_bound_bl(L, len, w) : lower_bound(L, len, w);
                         if (q < len && L[q] == w) {
                             TWC_ASSERT(r0 + j - A >= 0 && r0 + j - A < len);
-                            if (staged) {
-                                atomicAdd(&H.cnt[q], 1);             // t(u, w)
-                                atomicAdd(&H.cnt[r0 + j - A], 1);    // t(u, v)
-                            } else {
-                                atomicAdd(&t_or[A + q], 1);
-                                atomicAdd(&t_or[r0 + j], 1);
-                            }
+                            atomicAdd(&t_or[A + q], 1);              // t(u, w)
+                            atomicAdd(&t_or[r0 + j], 1);             // t(u, v)
                             atomicAdd(&t_or[sv], 1);                 // t(v, w)
                         }
                     }
@@ -786,11 +784,6 @@ __global__ void __launch_bounds__(kK2Warps * 32, 2) k2_hubs(
             }
         }
         __syncthreads();
-        if (staged)
-            for (int i = threadIdx.x; i < len; i += blockDim.x) {
-                const int c = H.cnt[i];
-                if (c) atomicAdd(&t_or[A + i], c);
-            }
         __syncthreads();
     }
 }
@@ -1143,7 +1136,7 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
     k2_find_hubs<<<(unsigned)((n + 255) / 256), 256, 0, sh>>>(n, w.rp_or, w.hubs, w.nhubs, range);
     const size_t hsmem = sizeof(K2HubSmem);
     kernel_setup((const void*)k2_hubs, kK2Warps * 32, hsmem);
-    k2_hubs<<<sms * 2, kK2Warps * 32, hsmem, sh>>>(w.rp_or, w.col_or, w.hubs, w.nhubs,
+    k2_hubs<<<sms * kHubMinBlocks, kK2Warps * 32, hsmem, sh>>>(w.rp_or, w.col_or, w.hubs, w.nhubs,
                                                     w.work + 1, w.t_or);
     if (ax) cudaEventRecord(ax->join, sh);
     // pivots per queue grab: kPivotChunk, fewer when there are too few pivots to give every

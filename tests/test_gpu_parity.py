@@ -105,7 +105,7 @@ def test_hub_closed_forms(rb):
 
 
 def test_hub_beyond_smem_staging():
-    """K_8300: the top pivots' oriented lists (up to 8,299) exceed the hub kernel's 8,192-entry
+    """K_8300: the top pivots' oriented lists (up to 8,299) exceed the hub kernel's 2,048-entry
     smem staging, so their candidates are verified in global memory (closed form t = n - 2)."""
     g = gg.complete(8300, np.int64)
     t, w, tw = gpu_score(g)

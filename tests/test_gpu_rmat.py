@@ -97,7 +97,7 @@ def check_sampled_rows(oracle_mod, g, t, w, tw, windows):
 def test_rmat_1e8_sampled_parity(oracle_mod, name):
     """P:736 / P:742 rows at 10^8 requested edges.  Sampled rows: low ids (the R-MAT hubs), the
     rows of the 8 pivots with the longest oriented lists (d-1e8: |N+(u)| up to 854, all handled
-    by the hub kernel K2h; no R-MAT list exceeds K2h's 8,192-entry staging, see
+    by the hub kernel K2h; no R-MAT list exceeds K2h's 2,048-entry staging, see
     test_dense_core_beyond_hub_staging), middle and high ids, a ragged end window."""
     oracle_mod.set_threads(oracle_mod.max_threads())
     g = gg.rmat_graph(name)
