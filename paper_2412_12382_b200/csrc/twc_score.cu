@@ -1062,12 +1062,18 @@ __global__ void k_dist_bounds(int64_t n, int64_t m, const int* __restrict__ rp_o
 // measured optimum; the filter / ring / group-cap / occupancy variants were
 // A/B-tested in round 2 and lost).
 constexpr int kK2FilterLog = 13;
-constexpr int kK2MinBlocks = 5;
+#ifndef TWC_K2_MINB
+#define TWC_K2_MINB 5
+#endif
+#ifndef TWC_K2_RING
+#define TWC_K2_RING kRing
+#endif
+constexpr int kK2MinBlocks = TWC_K2_MINB;
 #ifndef TWC_K2_SPL
 #define TWC_K2_SPL 1
 #endif
-#define K2_KERNEL k2_intersect<kOct, kK2FilterLog, kK2MinBlocks, kRing, TWC_K2_SPL>
-using K2Smem = K2WarpSmem<kK2FilterLog, kRing, TWC_K2_SPL>;
+#define K2_KERNEL k2_intersect<kOct, kK2FilterLog, kK2MinBlocks, TWC_K2_RING, TWC_K2_SPL>
+using K2Smem = K2WarpSmem<kK2FilterLog, TWC_K2_RING, TWC_K2_SPL>;
 
 
 // Stage A: degrees, orientation + oriented CSR (K0, K1) and the intersection (K2h, K2) of all
