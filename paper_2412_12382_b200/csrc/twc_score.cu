@@ -354,7 +354,7 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
 //  * filter position of w: word = top bits of x = w * K, bit = x & 31 (K odd, so x & 31 is a
 //    bijection of w & 31); one funnel rotate by (x - e) puts item e's bit at position e;
 //  * an item whose w misses the filter cannot be in N+(u) (the common case).  A lane with
-//    candidates pushes ONE record (slot of the quad, 4-bit mask, tag = slot u->v and pivot)
+//    candidates pushes ONE record (slot of the sector, 8-bit mask, tag = slot u->v and pivot)
 //    with one ballot; records are expanded into a candidate ring 32 at a time and candidates
 //    verified 32 at a time by binary search in the staged sorted N+(u), so the prefix work and
 //    the search run on full warps.  Record and candidate entries are self-contained, so the
@@ -363,7 +363,7 @@ __global__ void k1_rows(int64_t n, int64_t m, const RP* __restrict__ rowptr,
 //    first two land in the group's own slot range [A, B), a few sectors per verify batch).
 //    Per-warp shared byte counters were used before; K2 is bound by the L1/shared data pipe,
 //    and their atomics cost bank-conflict replays plus a flush per group;
-//  * the round setup prefetches each lane's N+(v) into L2, so the quad loop's loads find it.
+//  * the round setup prefetches each lane's N+(v) into L2, so the sector loop's loads find it.
 // DESIGN.md Sec. 4.1 lists the variants measured on the way (ncu evidence per step).
 constexpr int kK2Warps = 8;
 constexpr int kGroupSlots = 256;
@@ -384,7 +384,7 @@ struct K2WarpSmem {
     int prp[33];                    // ends of the group's non-empty lists (list j = [prp[j], prp[j+1]))
     int4 seg[32 * SPL];             // per slot of the round: {start of N+(v) - 8 * first sector, end, tag, start}
     int2 ring[RING];                // candidates: {slot of v -> w, tag}
-    int2 rec[kRec];                 // candidate quads: {slot of the quad, mask | tag << 4}
+    int2 rec[kRec];                 // candidate sectors: {slot of the sector, mask | tag << 8}
 };
 
 template <int FLOG>
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(kK2Warps * 32, MINB) k2_intersect(int64_t n, i
 // ------------------------------------------------------ K2h: hub pivots (|N+(u)| > 256)
 // One pivot per CTA: the whole block stages N+(u) (up to kHubMax entries) and a 64K-bit filter
 // of it in shared memory, and its 8 warps take the pivot's slots 32 at a time with the same
-// flattened-quad scan, filter and candidate ring as K2.  A list longer than kHubMax keeps only
+// flattened sector scan, filter and candidate ring as K2.  A list longer than kHubMax keeps only
 // the filter; its candidates are verified by binary search in global memory.
 constexpr int kHubMax = 2048;
 constexpr int kHubQ = 8;        // items per lane: one aligned 32-byte sector (one LDG.E.256)
