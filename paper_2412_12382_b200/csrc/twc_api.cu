@@ -3,6 +3,8 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <atomic>
@@ -72,6 +74,109 @@ int kernel_setup(const void* fn, int threads, size_t smem) {
     }
     cache.push_back({dev, fn, smem, occ});
     return occ;
+}
+
+// Persisting-L2 window for the per-vertex record array vinfo (8n bytes), which K2 gathers once
+// per oriented slot and K3 once per reversed edge.  Under the 5-6 TB/s of streaming traffic of
+// those kernels a normally cached line lives ~20 us in L2, about the interval between two uses
+// of a vinfo line, so most of those gathers went to DRAM (a 64-byte access each); eviction
+// hints on the loads did not change that.  With an L2 set-aside
+// (cudaLimitPersistingL2CacheSize, 32 MiB, set once per device on the first call that needs it)
+// and an access-policy window on the caller's stream from k1_rows (which writes vinfo) to K3,
+// the records stay in L2: config 5 K2 1.72 -> 1.68 ms, K3 0.87 -> 0.82 ms, DRAM reads -0.55 /
+// -0.34 GB.  24 / 40 / 48 MiB gain less and 64 MiB costs the other data too much L2 (step 4.5
+// ms).  The window is used only when the oriented arrays (col_or + t_or, 8m bytes) exceed the
+// L2: on smaller graphs everything stays cached anyway and the set-aside only cost capacity
+// (config 4: +3 %); such a call resets persisting lines an earlier large call left behind.
+// These are cache hints: results never depend on them.  TWC_L2_PERSIST_MB overrides the
+// set-aside size (0 = never use the window); a device without the feature, or a first call made
+// during stream capture (the limit cannot be set then), runs without it.
+#ifndef TWC_L2_PERSIST_DEFAULT_MB
+#define TWC_L2_PERSIST_DEFAULT_MB 32
+#endif
+namespace {
+struct L2Dev {
+    bool done = false;    // set-aside decided for this device
+    size_t cap = 0;       // set-aside bytes (0: window off)
+    size_t l2 = 0;        // L2 size
+    size_t max_win = 0;   // largest access-policy window
+    bool dirty = false;   // persisting lines of an earlier windowed call may still be resident
+};
+std::mutex g_l2_mu;
+L2Dev g_l2[64];
+}  // namespace
+
+static bool stream_capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return cs != cudaStreamCaptureStatusNone;
+}
+
+// returns the device's record with the set-aside decided, or nullptr (feature off / not yet)
+static L2Dev* l2_device(cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return nullptr;
+    L2Dev& d = g_l2[dev];
+    if (!d.done) {
+        if (stream_capturing(s)) return nullptr;  // decided by the first call outside a capture
+        d.done = true;
+        const char* e = getenv("TWC_L2_PERSIST_MB");
+        const long mb = e ? atol(e) : (long)TWC_L2_PERSIST_DEFAULT_MB;
+        int maxp = 0, maxw = 0, l2 = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        d.l2 = (size_t)std::max(l2, 0);
+        d.max_win = (size_t)std::max(maxw, 0);
+        if (mb > 0 && maxp > 0 && maxw > 0 && l2 > 0) {
+            const size_t want = std::min<size_t>((size_t)mb << 20, (size_t)maxp);
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
+                d.cap = want;
+        }
+        cudaGetLastError();
+    }
+    return d.cap ? &d : nullptr;
+}
+
+bool l2_window_begin(cudaStream_t s, const void* ptr, size_t bytes, size_t streamed_bytes) {
+    std::lock_guard<std::mutex> lock(g_l2_mu);
+    L2Dev* d = l2_device(s);
+    if (!d || !bytes || !ptr) return false;
+    if (streamed_bytes < d->l2) {  // everything stays cached without help
+        if (d->dirty && !stream_capturing(s)) {
+            cudaCtxResetPersistingL2Cache();
+            cudaGetLastError();
+            d->dirty = false;
+        }
+        return false;
+    }
+    cudaStreamAttrValue a;
+    memset(&a, 0, sizeof(a));
+    a.accessPolicyWindow.base_ptr = const_cast<void*>(ptr);
+    a.accessPolicyWindow.num_bytes = std::min(bytes, d->max_win);
+    a.accessPolicyWindow.hitRatio =
+        std::min(1.0f, (float)((double)d->cap / (double)a.accessPolicyWindow.num_bytes));
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    d->dirty = true;
+    return true;
+}
+
+void l2_window_end(cudaStream_t s) {
+    cudaStreamAttrValue a;
+    memset(&a, 0, sizeof(a));
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyNormal;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+    if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a) != cudaSuccess)
+        cudaGetLastError();
 }
 
 static twc_status check_csr(const twc_csr* g, bool need_ptrs = true, bool device_ptrs = true) {

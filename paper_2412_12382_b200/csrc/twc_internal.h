@@ -32,6 +32,11 @@ int num_sms();
 // SM (>= 1).  Thread-safe; the cache is the library's only process-wide state besides the
 // launch counter and the per-thread error string.
 int kernel_setup(const void* fn, int threads, size_t smem);
+// persisting-L2 access-policy window on stream s for [ptr, ptr + bytes), used when the call
+// streams more than the L2 holds (twc_api.cu); begin returns whether a window was set, and only
+// then must end be called
+bool l2_window_begin(cudaStream_t s, const void* ptr, size_t bytes, size_t streamed_bytes);
+void l2_window_end(cudaStream_t s);
 
 // Launch accounting (twc_kernel_launches) and optional phase events (twc_*_ex).
 void count_launches(int k);

@@ -1079,12 +1079,13 @@ using K2Smem = K2WarpSmem<kK2FilterLog, TWC_K2_RING, TWC_K2_SPL>;
 // Stage A: degrees, orientation + oriented CSR (K0, K1) and the intersection (K2h, K2) of all
 // pivots, or of a shard's pivot range.  Events [0] start, [1] orientation done, [2] K2 done.
 template <typename RP>
-static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
+static bool stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const int* colidx,
                                    const ScoreWs& w, cudaStream_t s, cudaEvent_t* ev,
                                    const ShardSpec* shard, int* parent = nullptr) {
     const int sms = num_sms();
     const int64_t m2 = 2 * m;
     const int64_t nst = (m2 + kSlotTile - 1) / kSlotTile;
+    bool win = false;
     record(ev, 0, s);
     // the oriented counts and the queue counters are zeroed on the library's side stream while K1
     // runs (K1 is bound by its deg gathers, not by DRAM; the 4m-byte memset took 25 us between K1
@@ -1108,6 +1109,9 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
         k1_tile_scan<<<1, 1024, 0, s>>>(nst, w.tile_out, w.tile_up);
         k1_write<<<grid, kSlotThreads, 0, s>>>(m2, colidx, w.obits, w.ubits, w.tile_out,
                                                w.tile_up, w.opre, w.upre, w.col_or);
+        // vinfo (written here, gathered by K2 and K3) stays in the persisting part of L2 until the
+        // caller ends the window after K3 (twc_api.cu l2_window_begin; large graphs only)
+        win = l2_window_begin(s, w.vinfo, sizeof(int2) * (size_t)n, 2 * sizeof(int) * (size_t)m);
         k1_rows<RP><<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, m, rowptr, w.obits, w.ubits,
                                                                    w.opre, w.upre, w.rp_or, w.eoff,
                                                                    w.vinfo);
@@ -1154,6 +1158,7 @@ static void stage_orient_intersect(int64_t n, int64_t m, const RP* rowptr, const
     if (ax) cudaStreamWaitEvent(s, ax->join, 0);
     count_launches(3);
     record(ev, 2, s);
+    return win;  // an L2 window on vinfo is open on s: the caller ends it
 }
 
 template <typename RP>
@@ -1164,14 +1169,18 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
     Carver cv(ws, ws_bytes);
     ScoreWs w = carve_score(cv, n, m);
     const int sms = num_sms();
-    stage_orient_intersect<RP>(n, m, rowptr, colidx, w, s, ev, nullptr, bin ? bin->parent : nullptr);
+    const bool win = stage_orient_intersect<RP>(n, m, rowptr, colidx, w, s, ev, nullptr,
+                                                bin ? bin->parent : nullptr);
     // NEXT(4): K4 participation on the same oriented CSR (workspace after the score's)
     unsigned long long* k4_or = nullptr;
     if (k4) {
         const size_t used = score_ws_bytes(n, m);
         cudaError_t e = k4_count(n, m, w.rp_or, w.col_or, static_cast<char*>(ws) + used,
                                  ws_bytes - used, &k4_or, s);
-        if (e != cudaSuccess) return e;
+        if (e != cudaSuccess) {
+            if (win) l2_window_end(s);
+            return e;
+        }
     }
     // a4: canonical gather + wedge + TW
     {
@@ -1190,6 +1199,7 @@ cudaError_t score_impl(int64_t n, int64_t m, const RP* rowptr, const int* colidx
                 n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits, w.t_or, t,
                 wedge, tw, BinSpec{});
         count_launches(1);
+        if (win) l2_window_end(s);
         record(ev, 3, s);
     }
     return cudaGetLastError();
@@ -1201,7 +1211,7 @@ cudaError_t dist_stage_a(int64_t n, int64_t m, const RP* rowptr, const int* coli
     Carver cv(ws, ws_bytes);
     ScoreWs w = carve_score(cv, n, m);
     const ShardSpec sh{rank, world, bounds};
-    stage_orient_intersect<RP>(n, m, rowptr, colidx, w, s, nullptr, &sh);
+    if (stage_orient_intersect<RP>(n, m, rowptr, colidx, w, s, nullptr, &sh)) l2_window_end(s);
     return cudaGetLastError();
 }
 
@@ -1212,9 +1222,12 @@ cudaError_t dist_epilogue(int64_t n, int64_t m, const RP* rowptr, const int* col
     Carver cv(ws, ws_bytes);
     ScoreWs w = carve_score(cv, n, m);
     const int grid = grid_for(num_tiles(m), 1, num_sms() * 8);
+    const bool win =
+        l2_window_begin(s, w.vinfo, sizeof(int2) * (size_t)n, 2 * sizeof(int) * (size_t)m);
     k3_score<RP, true, false, true><<<grid, kK3Threads, k3_bin_smem(bin.k), s>>>(
         n, m, rowptr, colidx, w.vinfo, w.dslot, w.deg, w.eoff, w.trow, w.col_or, w.opre, w.obits,
         w.t_or, t, wedge, tw, bin, nullptr, nullptr, d);
+    if (win) l2_window_end(s);
     count_launches(1);
     return cudaGetLastError();
 }

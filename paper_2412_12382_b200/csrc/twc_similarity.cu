@@ -19,12 +19,41 @@ namespace twc {
 constexpr int kSimThreads = 256;
 constexpr int kSimTileRows = 2048;
 
+// #upper(u) = #{v in N(u): v > u} and, for the degree kinds, deg[u] (one pass over rowptr)
 template <typename RP>
-__global__ void k_sim_degrees(int64_t n, const RP* __restrict__ rowptr, int* __restrict__ deg) {
+__global__ void k_sim_rows(int64_t n, const RP* __restrict__ rowptr,
+                           const int* __restrict__ colidx, int* __restrict__ up,
+                           int* __restrict__ deg) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u < n) deg[u] = (int)(rowptr[u + 1] - rowptr[u]);
+    if (u >= n) return;
+    const RP beg = rowptr[u];
+    const int d = (int)(rowptr[u + 1] - beg);
+    up[u] = d - lower_bound(colidx + beg, d, (int)u);  // rows are strictly increasing
+    deg[u] = d;
 }
 
+__device__ __forceinline__ double sim_value(int kind, long long tt, long long dsum) {
+    switch (kind) {
+        case 0: return (double)(3 * tt - dsum + 2);
+        case 1: return (double)tt / (double)dsum;
+        case 2: return (double)tt / (double)(dsum - tt);
+        case 3: return (double)tt;
+        default: return -2.0 / (2.0 + (double)tt);
+    }
+}
+
+// kinds K3 and -R_eff depend on t alone: a streaming pass (12 bytes per edge), no CSR
+__global__ void __launch_bounds__(kSimThreads) k_similarity_t(int64_t m, const int* __restrict__ t,
+                                                              int kind, double* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += stride)
+        __stcs(out + c, sim_value(kind, (long long)__ldcs(t + c), 0));
+}
+
+// The degree kinds (TW, Tectonic, Jaccard), one canonical edge per thread and tile pass.  (A
+// variant with four consecutive edges per thread -- one row search and a walk, 16-byte reads
+// of t and 32-byte writes -- was measured slower: 0.55-0.60 ms against 0.42-0.47 ms on config
+// 5, 48 registers and four scalar colidx reads per thread into the same sectors.)
 // The far endpoint's degree comes from a 4-byte deg[] (16 MB for config 5, L2-resident) rather
 // than from two 8-byte rowptr reads of a 32 MB array: one random L2 sector per edge.
 template <typename RP>
@@ -54,15 +83,7 @@ __global__ void __launch_bounds__(kSimThreads) k_similarity(
             const int v = colidx[rb + (RP)(du - upu) + (RP)(c - eu)];
             const long long dv = (long long)deg[v];
             const long long tt = t[c];
-            double x;
-            switch (kind) {
-                case 0: x = (double)(3 * tt - du - dv + 2); break;
-                case 1: x = (double)tt / (double)(du + dv); break;
-                case 2: x = (double)tt / (double)(du + dv - tt); break;
-                case 3: x = (double)tt; break;
-                default: x = -2.0 / (2.0 + (double)tt); break;
-            }
-            out[c] = x;
+            out[c] = sim_value(kind, tt, du + dv);
         }
     }
 }
@@ -72,6 +93,13 @@ cudaError_t similarity_impl(int64_t n, int64_t m, const RP* rowptr, const int* c
                             const int* t, int kind, void* ws, size_t ws_bytes, double* out,
                             cudaStream_t s) {
     if (m == 0 || n == 0) return cudaGetLastError();
+    if (kind == 3 || kind == 4) {
+        const int grid = (int)std::min<int64_t>((m + kSimThreads - 1) / kSimThreads,
+                                                (int64_t)num_sms() * 16);
+        k_similarity_t<<<grid, kSimThreads, 0, s>>>(m, t, kind, out);
+        count_launches(1);
+        return cudaGetLastError();
+    }
     // reuse the cluster workspace layout for the canonical offsets: up, eoff, scan, tile rows
     Carver cv(ws, ws_bytes);
     int* up = cv.take<int>(n);
@@ -79,10 +107,9 @@ cudaError_t similarity_impl(int64_t n, int64_t m, const RP* rowptr, const int* c
     int* scan_tmp = cv.take<int>(scan_temp_bytes(n) / sizeof(int));
     int* trow = cv.take<int>(num_tiles(m) + 1);
     int* deg = cv.take<int>(n);
-    upper_counts<RP>(n, rowptr, colidx, up, s);
+    k_sim_rows<RP><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rowptr, colidx, up, deg);
     exclusive_scan(up, eoff, n, scan_tmp, s);
     tile_first_rows(eoff, (int)n, m, trow, s);
-    k_sim_degrees<RP><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rowptr, deg);
     const int grid = (int)std::min<int64_t>(num_tiles(m), (int64_t)num_sms() * 8);
     k_similarity<RP><<<grid, kSimThreads, 0, s>>>(m, rowptr, colidx, eoff, trow, deg, t, kind,
                                                   out);

@@ -91,10 +91,12 @@ def main():
             for kind in twc.SIM_KINDS:
                 ms = timed(lambda: twc.twc_similarity(rp, ci, t, kind, out=score, workspace=wsc),
                            flush)
+                # degree kinds: t, colidx, deg(u) + deg(v), the 8-byte score; K3 / -R_eff read t only
+                bpe = 4 + 8 if kind in ("k3", "effres") else 4 + 8 + 8 + 4
                 line = {"what": "similarity", "graph": name, "kind": kind, "ms": ms,
                         "edges_per_s": m / (ms / 1e3),
-                        "bytes_per_edge_model": 4 + 8 + 8 + 4,
-                        "achieved_gbs_model": m * 24 / (ms / 1e3) / 1e9}
+                        "bytes_per_edge_model": bpe,
+                        "achieved_gbs_model": m * bpe / (ms / 1e3) / 1e9}
                 print(json.dumps(line), flush=True)
                 res.append(line)
         del rp, ci, ws, out

@@ -95,3 +95,25 @@ def test_proposition_1_on_gpu(oracle_mod):
         lj, sj = twc.twc_sweep_f64(rp, ci, jac, [dj])
         lt, st = twc.twc_sweep_f64(rp, ci, tec, [dj / (1 + dj)])
         assert torch.equal(lj, lt) and torch.equal(sj, st), k
+
+
+def test_similarity_unaligned_buffers_and_ragged_tail(oracle_mod):
+    """t and the score array need only their natural alignment (views shifted by one element,
+    4 / 8 bytes off a 16-byte boundary), for the streaming kinds (K3, -R_eff: no CSR read) and
+    the degree kinds alike; m not a multiple of the 1,024-edge tile exercises the ragged tail."""
+    for n, p, seed in ((700, 0.03, 3), (2500, 0.004, 4), (1203, 0.011, 5)):
+        g = gg.erdos_renyi(n, p, seed=seed)
+        rp, ci = harness.to_device(g)
+        t, _, _ = twc.twc_score(rp, ci)
+        ot, _, _ = oracle_mod.score(g)
+        m = int(t.numel())
+        tbuf = torch.empty(m + 1, dtype=torch.int32, device=t.device)
+        tbuf[1:].copy_(t)
+        obuf = torch.empty(m + 1, dtype=torch.float64, device=t.device)
+        for kind in KINDS:
+            os_ = oracle_mod.similarity(g, ot, kind)
+            got = twc.twc_similarity(rp, ci, tbuf[1:], kind, out=obuf[1:])
+            assert got.data_ptr() % 16 == 8 and tbuf[1:].data_ptr() % 16 == 4
+            assert np.array_equal(got.cpu().numpy(), os_), (kind, m)
+            got = twc.twc_similarity(rp, ci, t, kind)
+            assert np.array_equal(got.cpu().numpy(), os_), (kind, m)
