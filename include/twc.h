@@ -45,6 +45,16 @@
  *           the launch counter of twc_kernel_launches(), per-(thread, device) side/copy streams
  *           and events created on first use, and a mutex-guarded per-(device, kernel) cache of
  *           the dynamic-shared-memory attribute and occupancy (the attribute is per device).
+ *  L2.      The first scoring call on a device whose graph's oriented arrays (8m bytes) exceed
+ *           the L2 sets that device's persisting-L2 set-aside to 32 MiB
+ *           (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize); environment TWC_L2_PERSIST_MB
+ *           overrides the size, 0 = never).  Such calls put an access-policy window on `stream`
+ *           around their intersection and epilogue kernels (the per-vertex record array the
+ *           kernels gather from stays in L2) and clear the stream's window before they return,
+ *           so a window the caller had set on `stream` is not preserved.  A later call on a small
+ *           graph resets the persisting lines (cudaCtxResetPersistingL2Cache).  These are cache
+ *           hints only: results never depend on them, and a device without the feature, or a
+ *           first call made during stream capture, simply runs without the window.
  */
 #ifndef TWC_H_
 #define TWC_H_
