@@ -79,8 +79,8 @@ int kernel_setup(const void* fn, int threads, size_t smem) {
 // Persisting-L2 window for the per-vertex record array vinfo (8n bytes), which K2 gathers once
 // per oriented slot and K3 once per reversed edge.  Under the 5-6 TB/s of streaming traffic of
 // those kernels a normally cached line lives ~20 us in L2, about the interval between two uses
-// of a vinfo line, so most of those gathers went to DRAM (a 64-byte access each); eviction
-// hints on the loads did not change that.  With an L2 set-aside
+// of a vinfo line, so a good part of those gathers went to DRAM (a 64-byte access each);
+// eviction hints on the loads did not change that.  With an L2 set-aside
 // (cudaLimitPersistingL2CacheSize, 32 MiB, set once per device on the first call that needs it)
 // and an access-policy window on the caller's stream from k1_rows (which writes vinfo) to K3,
 // the records stay in L2: config 5 K2 1.72 -> 1.68 ms, K3 0.87 -> 0.82 ms, DRAM reads -0.55 /
